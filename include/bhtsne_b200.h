@@ -1,0 +1,242 @@
+/*
+ * bhtsne_b200.h -- C ABI of the B200-native Barnes-Hut t-SNE hot path.
+ *
+ * One shared library (paper_2212_11506_b200/libbhtsne_b200.so, sm_100a) that
+ * replaces the numba kernels behind the reference package's stage functions
+ * (reference: /root/reference/pkg/src/bhtsne/, exported at __init__.py:22-84).
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Every pointer argument is DEVICE memory allocated by the caller (the
+ *    Python host uses torch tensors).  The library never allocates, frees or
+ *    retains caller memory.
+ *  - Scratch comes from the caller: query `bh_*_workspace_bytes`, allocate
+ *    that many bytes ZERO-FILLED once, and pass it back on every call.  The
+ *    library leaves all counters it keeps there at zero on return, so a
+ *    workspace can be reused across calls and CUDA-graph replays.
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t; NULL = the
+ *    legacy default stream), never synchronises the host, and returns BH_OK
+ *    (0) or a negative BH_ERR_* code; `bh_last_error()` (thread-local) then
+ *    holds a message.
+ *  - Point coordinates are float32 (N, 2) row-major ("(y0, y1)" pairs), the
+ *    reference's f32 run mode (io.py:21-30).  Accumulations are float64, as
+ *    in the reference kernels.
+ *  - Morton codes are 32-bit (16 bits per dimension, tree depth <= 16) by
+ *    default or 64-bit (the reference's own width, depth <= 32): `code_bits`.
+ */
+#ifndef BHTSNE_B200_H
+#define BHTSNE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BH_ABI_VERSION 1
+
+enum {
+    BH_OK = 0,
+    BH_ERR_ARG = -1,         /* invalid argument (message in bh_last_error) */
+    BH_ERR_CUDA = -2,        /* a CUDA launch/runtime error */
+    BH_ERR_CAPACITY = -3,    /* caller buffer too small */
+    BH_ERR_UNSUPPORTED = -5, /* e.g. a code width other than 32/64 */
+};
+
+typedef void *bh_stream_t; /* cudaStream_t */
+
+/* Bounding square + Morton constants, resident on the device.
+ * c0, c1, r_span: compute_bounds (quadtree.py:133-153), computed in f64
+ * exactly as the reference.  root0/root1/scale: _morton_kernel's constants
+ * (quadtree.py:179-181) for `code_bits`.  shift0/shift1: a pending
+ * re-centering (optimizer.py:220-221) that bh_morton applies when asked;
+ * bounds already describe the re-centred points.  nonfinite: set to 1 when a
+ * coordinate was NaN/Inf (quadtree.py:143-144). */
+typedef struct bh_bounds {
+    double c0, c1, r_span;
+    double root0, root1, scale;
+    float shift0, shift1;
+    int32_t nonfinite;
+    int32_t code_bits;
+} bh_bounds;
+
+/* Optimiser schedule, resident on the device so that whole iterations can be
+ * captured in one CUDA graph.  Mirrors TsneConfig (optimizer.py:43-57) and
+ * the run() schedule (optimizer.py:316-321): exaggeration applies while
+ * iteration < exaggeration_iters, momentum_early while iteration <
+ * momentum_switch (MOMENTUM_SWITCH_ITER = 250, optimizer.py:40).
+ * `bad` = (iteration << 32 | point) of the first non-finite gradient
+ * (optimizer.py:208-211), INT64_MAX while none; `z` = the last Z. */
+typedef struct bh_sched {
+    int32_t iteration;
+    int32_t exaggeration_iters;
+    int32_t momentum_switch;
+    int32_t pad0;
+    float exaggeration;
+    float momentum_early, momentum_late;
+    float learning_rate, min_gain;
+    float pad1;
+    int64_t bad;
+    double z;
+} bh_sched;
+
+/* Node record of the level-contiguous quadtree (16 bytes):
+ *   x, y  : centre of mass (float32, quadtree.py:488-508)
+ *   mass  : point count (uint32 bits)
+ *   info  : bit 31 = leaf; leaf -> bits 0..30 = first point (sorted order);
+ *           internal -> bits 0..28 = first child node, bits 29..30 =
+ *           (number of children - 1).  Children of a node are consecutive
+ *           in the next level, in Morton-digit order (quadtree.py:66-85). */
+#define BH_LEAF_BIT 0x80000000u
+#define BH_CHILD_MASK 0x1FFFFFFFu
+#define BH_NKIDS_SHIFT 29
+
+/* Quadtree arrays (caller-allocated; capacity = n * (max_depth + 1) + 1 is
+ * always sufficient, bh_tree_node_bound()).  Replaces MortonQuadtree
+ * (quadtree.py:66-85). */
+typedef struct bh_tree {
+    int64_t n_points;
+    int64_t node_capacity;
+    int32_t code_bits; /* 32 or 64 */
+    int32_t max_depth; /* code_bits / 2 */
+    float *node;       /* 4 * node_capacity floats: records as above */
+    int32_t *parent;   /* node_capacity: parent node, -1 for the root */
+    int32_t *node_start; /* node_capacity: first point (sorted order) */
+    int32_t *leaf_end;   /* node_capacity: one past the last point (leaves) */
+    uint32_t *nkids;     /* node_capacity scratch, zero on entry and exit */
+    uint32_t *arrive;    /* node_capacity scratch, zero on entry and exit */
+    int32_t *level_off;  /* max_depth + 3 entries: level l = [off[l], off[l+1]),
+                            off[max_depth + 2] = number of levels */
+    int32_t *order;      /* n: sorted position -> point id */
+    void *sorted_codes;  /* n codes (uint32 or uint64) */
+    float *ys;           /* 2n: coordinates in sorted order (quadtree.py:476) */
+    int32_t *pt_leaf;    /* n: the leaf whose first point is t, else -1 */
+    int32_t *status;     /* device int32: BH_OK or BH_ERR_CAPACITY after build */
+} bh_tree;
+
+const char *bh_last_error(void);
+int bh_abi_version(void);
+int64_t bh_tree_node_bound(int64_t n, int code_bits);
+
+/* ---- bounds + Morton codes: compute_bounds / morton_codes --------------
+ * quadtree.py:133-153, 177-185, 230-242. */
+size_t bh_bounds_workspace_bytes(int64_t n);
+int bh_bounds(const float *y, int64_t n, int code_bits, bh_bounds *out,
+              void *ws, size_t ws_bytes, bh_stream_t stream);
+/* codes[i] for point i; apply_shift: first re-centre y in place by
+ * (shift0, shift1) (the fused update/centering of gradient_step). */
+int bh_morton(float *y, int64_t n, const bh_bounds *bounds, int code_bits,
+              int apply_shift, void *codes, bh_stream_t stream);
+
+/* ---- stable radix sort: _radix_argsort (quadtree.py:188-227) ------------
+ * Sorts keys (uint32 when key_bits <= 32, else uint64) with ids 0..n-1 as
+ * payload, stable, over bits [0, key_bits).  Equivalent to
+ * np.argsort(keys, kind="stable") (test_quadtree.py:97-99). */
+size_t bh_sort_workspace_bytes(int64_t n, int key_bits);
+int bh_sort(const void *keys, int64_t n, int key_bits, void *sorted_keys,
+            int32_t *order, void *ws, size_t ws_bytes, bh_stream_t stream);
+/* Same, with an explicit uint32 payload (used by the CSR builder). */
+int bh_sort_pairs(const void *keys, const uint32_t *vals, int64_t n,
+                  int key_bits, void *sorted_keys, uint32_t *sorted_vals,
+                  void *ws, size_t ws_bytes, bh_stream_t stream);
+
+/* ---- tree build: build_tree (quadtree.py:399-478) -----------------------
+ * Single-pass ballot-scan builder over the sorted codes; bit-identical
+ * topology to the reference builder at the same depth.  Also gathers
+ * ys = y[order].  On overflow of node_capacity, *tree->status is set to
+ * BH_ERR_CAPACITY and the tree is left incomplete. */
+size_t bh_tree_workspace_bytes(int64_t n, int code_bits);
+int bh_build_tree(const bh_tree *tree, const float *y, void *ws,
+                  size_t ws_bytes, bh_stream_t stream);
+
+/* ---- summarize (quadtree.py:481-519) --------------------------------------
+ * Bottom-up centre of mass and count; bit-identical to the reference
+ * (f64 sums in reference order, stored as float32). */
+int bh_summarize(const bh_tree *tree, bh_stream_t stream);
+
+/* ---- attractive force (forces.py:56-82) ---------------------------------
+ * attr[i] = sum_t v_t*(y_i - y_j)/(1+|y_i-y_j|^2) over CSR row i, for rows
+ * [row_begin, row_end).  v_t is scaled by the exaggeration: `sched` (if not
+ * NULL) selects it from the schedule, else `exaggeration` is used.
+ * `row_ptr` may be padded (rows start at multiples of 4 entries, pad
+ * entries have val 0): set padded=1 to use 128-bit loads. */
+int bh_attractive(const int64_t *row_ptr, const int32_t *col,
+                  const float *val, int64_t n_rows, int padded,
+                  const float *y, int64_t row_begin, int64_t row_end,
+                  float exaggeration, const bh_sched *sched, float *attr,
+                  bh_stream_t stream);
+
+/* ---- repulsive Barnes-Hut force (forces.py:85-150) -----------------------
+ * Warp-synchronous traversal over sorted positions [t_begin, t_end) with
+ * per-lane acceptance masks (the exact per-point BH semantics of the
+ * reference).  Writes rep[id] (float32 pairs, by point id), zpart[id]
+ * (float64, optional) and the fixed-order reduction of Z over the range
+ * into *z_out (optional).  `counts` (optional, 4 int32 per point id):
+ * internal visits, leaf-node visits, leaf points touched, accepted. */
+size_t bh_repulsive_workspace_bytes(int64_t n);
+int bh_repulsive(const bh_tree *tree, const bh_bounds *bounds, double theta,
+                 int64_t t_begin, int64_t t_end, float *rep, double *zpart,
+                 double *z_out, int32_t *counts, void *ws, size_t ws_bytes,
+                 bh_stream_t stream);
+
+/* ---- exact O(N^2) repulsion (forces.py:153-182) -------------------------- */
+size_t bh_repulsive_exact_workspace_bytes(int64_t n);
+int bh_repulsive_exact(const float *y, int64_t n, float *rep, double *zpart,
+                       double *z_out, void *ws, size_t ws_bytes,
+                       bh_stream_t stream);
+
+/* ---- KL divergence rows (optimizer.py:227-239) ---------------------------
+ * *kl_out = sum_i sum_t p ln(p Z (1+d^2)) with Z read from *z (device). */
+size_t bh_kl_workspace_bytes(int64_t n);
+int bh_kl_rows(const int64_t *row_ptr, const int32_t *col, const float *val,
+               int64_t n, int padded, const float *y, const double *z,
+               double *kl_out, void *ws, size_t ws_bytes, bh_stream_t stream);
+
+/* ---- momentum / gains update (optimizer.py:161-168, 195-224) -------------
+ * grad = 4 (attr - rep / f32(Z)); gains, velocity, y += v, then the mean of
+ * the new y is computed (f64) and published, with the bounds of the
+ * re-centred points, into *bounds_out (shift0/shift1 = the f32 mean).  The
+ * re-centering itself is applied by bh_center or by the next bh_morton
+ * (apply_shift=1).  Increments sched->iteration. */
+size_t bh_update_workspace_bytes(int64_t n);
+int bh_update(float *y, float *v, float *g, const float *attr,
+              const float *rep, int64_t n, bh_sched *sched,
+              bh_bounds *bounds_out, int code_bits, void *ws, size_t ws_bytes,
+              bh_stream_t stream);
+int bh_center(float *y, int64_t n, const bh_bounds *bounds,
+              bh_stream_t stream);
+
+/* ---- binary-search perplexity: calibrate_perplexity (affinity.py:61-118) --
+ * One warp per row, f64 bisection with the reference's exact schedule. */
+int bh_bsp(const float *sqd, int64_t n, int64_t k, double perplexity,
+           double tol_bits, int64_t max_iter, double *betas, double *cond,
+           bh_stream_t stream);
+
+/* ---- symmetrize (affinity.py:121-158) ------------------------------------
+ * p_ij = max((p_j|i + p_i|j) / 2N, eps64) as float32 CSR with ascending
+ * columns.  Two calls: bh_symmetrize_plan sorts the 2NK directed entries and
+ * writes the nnz to *nnz_out (device int64); after the caller allocates the
+ * outputs, bh_symmetrize_fill writes row_ptr (n+1), col and val (nnz). */
+size_t bh_symmetrize_workspace_bytes(int64_t n, int64_t k);
+int bh_symmetrize_plan(const int64_t *indices, int64_t n, int64_t k,
+                       int64_t *nnz_out, void *ws, size_t ws_bytes,
+                       bh_stream_t stream);
+int bh_symmetrize_fill(const double *cond, int64_t n, int64_t k,
+                       int64_t *row_ptr, int32_t *col, float *val, void *ws,
+                       size_t ws_bytes, bh_stream_t stream);
+/* Pads a CSR so every row starts at a multiple of 4 entries (pad entries:
+ * col = row, val = 0).  out_row_ptr has n+1 entries; out capacity from
+ * bh_pad_csr_size (device int64 result in *padded_nnz). */
+size_t bh_pad_csr_workspace_bytes(int64_t n);
+int bh_pad_csr_size(const int64_t *row_ptr, int64_t n, int64_t *out_row_ptr,
+                    int64_t *padded_nnz, void *ws, size_t ws_bytes,
+                    bh_stream_t stream);
+int bh_pad_csr_fill(const int64_t *row_ptr, const int32_t *col,
+                    const float *val, int64_t n, const int64_t *out_row_ptr,
+                    int32_t *out_col, float *out_val, bh_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BHTSNE_B200_H */
