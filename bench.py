@@ -1,0 +1,465 @@
+"""Benchmark: BH t-SNE gradient iterations/sec at N=1.3M (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c2|c1|c0] [--preroll R]
+
+A step is one gradient iteration (tree build, summarize, attractive,
+repulsive, update) of the full N=1.3M, D=50, K=90 problem (config C3,
+synthetic data: BASELINE.json configs[3]), on the device
+with inputs resident in HBM.  The timed region covers iterations
+[R+W, R+W+K) of the real 1000-iteration schedule (exaggeration 12 for 250,
+momentum 0.5 -> 0.8).  Setup (synthetic data, kNN graph via torch/cuBLAS,
+perplexity calibration via the CPU oracle, symmetrisation via a torch sort)
+is identical for both arms and cached in /tmp to spare the second arm.
+
+Prints ONE JSON line on rank 0 (see README of the driver contract): value =
+whole-job iterations/s, e2e = the same through the public host-buffer API,
+roofline of the dominant kernel, cpu_baseline = the CPU oracle (OpenMP
+restatement of the reference) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CACHE = "/tmp/bh_bench_cache"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# problem setup (identical for both arms)
+# ---------------------------------------------------------------------------
+def knn_torch(x: np.ndarray, k: int, dev):
+    """kNN graph for the benchmark inputs (setup only): fp32 distances via
+    cuBLAS, top-k per row; ascending, self excluded."""
+    import torch
+    xt = torch.from_numpy(x).to(dev)
+    n = xt.shape[0]
+    sq = (xt * xt).sum(1)
+    idx = torch.empty((n, k), dtype=torch.int64, device=dev)
+    sqd = torch.empty((n, k), dtype=torch.float32, device=dev)
+    chunk = 2048
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        d = sq[s:e, None] + sq[None, :] - 2.0 * (xt[s:e] @ xt.T)
+        d[torch.arange(e - s, device=dev), torch.arange(s, e, device=dev)] = float("inf")
+        v, i = torch.topk(d, k, dim=1, largest=False, sorted=True)
+        idx[s:e] = i
+        sqd[s:e] = v.clamp_min(0.0)
+    return idx.cpu().numpy(), sqd.cpu().numpy()
+
+
+def symmetrize_torch(indices, cond, dev):
+    """affinity.py:121-158 semantics with a device sort (setup only)."""
+    import torch
+    n, k = indices.shape
+    idx = torch.from_numpy(indices).to(dev)
+    c = torch.from_numpy(cond).to(dev).reshape(-1)
+    rows = torch.arange(n, device=dev).repeat_interleave(k)
+    cols = idx.reshape(-1)
+    key = torch.cat([rows * n + cols, cols * n + rows])
+    val = torch.cat([c, c])
+    key, order = torch.sort(key, stable=True)
+    val = val[order]
+    first = torch.ones_like(key, dtype=torch.bool)
+    first[1:] = key[1:] != key[:-1]
+    seg = torch.cumsum(first.to(torch.int64), 0) - 1
+    nnz = int(seg[-1].item()) + 1
+    summed = torch.zeros(nnz, dtype=torch.float64, device=dev)
+    summed.index_add_(0, seg, val)
+    uk = key[first]
+    vals = torch.clamp(summed / (2.0 * n), min=np.finfo(np.float64).eps)
+    ro = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    ro[1:] = torch.cumsum(torch.bincount(uk // n, minlength=n), 0)
+    return (ro.cpu().numpy(), (uk % n).to(torch.int32).cpu().numpy(),
+            vals.to(torch.float32).cpu().numpy())
+
+
+def problem(config: str, dev):
+    """Returns dict(n, row_offsets, col (int32), val (f32), y0 (N,2))."""
+    os.makedirs(CACHE, exist_ok=True)
+    path = os.path.join(CACHE, f"{config}_v1.npz")
+    if os.path.exists(path):
+        try:
+            with np.load(path) as z:
+                return {k: z[k] for k in z.files}
+        except Exception:
+            pass
+    from paper_2212_11506_b200 import workloads
+    from oracle import oracle as o
+    t0 = time.time()
+    spec = workloads.CONFIGS[config]
+    x = spec["gen"]()
+    log(f"[setup] {config}: data {x.shape} in {time.time() - t0:.1f}s")
+    t0 = time.time()
+    idx, sqd = knn_torch(x, 90, dev)
+    log(f"[setup] kNN (torch) {time.time() - t0:.1f}s")
+    t0 = time.time()
+    o.set_threads(0)
+    betas, cond = o.calibrate_perplexity(sqd, 30.0)
+    log(f"[setup] BSP (oracle) {time.time() - t0:.1f}s")
+    t0 = time.time()
+    ro, co, va = symmetrize_torch(idx, cond, dev)
+    log(f"[setup] symmetrize (torch) {time.time() - t0:.1f}s nnz={co.shape[0]}")
+    y0 = np.column_stack(o.init_embedding(x.shape[0], 0)).astype(np.float32)
+    out = dict(n=np.array(x.shape[0]), row_offsets=ro, col=co, val=va, y0=y0)
+    try:
+        np.savez(path + ".tmp.npz", **out)
+        os.replace(path + ".tmp.npz", path)
+    except OSError:
+        pass
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,"
+              "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}",
+                 f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4)
+                          if len(r) > 5 + j and r[5 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference restatement) timing
+# ---------------------------------------------------------------------------
+def cpu_oracle_time(prob, y, steps, code_bits=32):
+    """Full oracle gradient iterations on the host cores from state y."""
+    from oracle import oracle as o
+    threads = o.set_threads(0)
+    n = int(prob["n"])
+    s = o.State(np.ascontiguousarray(y[:, 0]), np.ascontiguousarray(y[:, 1]),
+                np.zeros(n, np.float32), np.zeros(n, np.float32),
+                np.ones(n, np.float32), np.ones(n, np.float32), 0)
+    ro = prob["row_offsets"]
+    co = prob["col"].astype(np.int64)
+    va = prob["val"]
+    stage = np.zeros(5)
+    tot = np.zeros(5)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.gradient_step(s, ro, co, va, code_bits=code_bits, stage_s=stage)
+        tot += stage
+    dt = time.perf_counter() - t0
+    return dt, threads, dict(zip(("tree", "summarize", "attractive",
+                                  "repulsive", "update"), (tot / steps).tolist()))
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# arms
+# ---------------------------------------------------------------------------
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    import torch
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else None
+    prob = problem(args.config, dev)
+    n = int(prob["n"])
+    y = prob["y0"]
+    w = min(args.warmup, 1)
+    steps = max(1, min(args.steps, args.ref_max_steps))
+    if w:
+        cpu_oracle_time(prob, y, w)
+    dt, threads, stages = cpu_oracle_time(prob, y, steps)
+    v = steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "it/s",
+        "n_gpus": world, "steps": steps, "warmup": w,
+        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_dict(args, n, int(prob["col"].shape[0])),
+        "cpu_baseline": {"value": v, "unit": "it/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{steps} full gradient iteration(s) of "
+                                   f"{args.config} from Y0 on {threads} threads "
+                                   f"({cpu_model()}); requested steps capped "
+                                   f"at {args.ref_max_steps}",
+                         "stage_s": stages},
+        "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "BH t-SNE gradient iters/sec at N=1.3M (1/2/4/8 B200); % of HBM roofline"
+
+
+def config_dict(args, n, nnz):
+    return {"workload": f"{args.config}: N={n}, D=50, K=90, perplexity 30, "
+                        f"theta {args.theta}, 1000-iteration schedule "
+                        f"(exaggeration 12 x 250), 32-bit Morton codes",
+            "n_points": n, "nnz": nnz, "theta": args.theta,
+            "timed_iterations": [args.preroll + args.warmup,
+                                 args.preroll + args.warmup + args.steps],
+            "l2": "inputs larger than L2 (CSR P alone > 126 MB); no flush",
+            "parallelism": f"dp{args.gpus} (points/rows sharded, tree replicated)"}
+
+
+def ours_arm(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2212_11506_b200 as bh
+    from paper_2212_11506_b200 import _lib
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    prob = problem(args.config, dev)
+    n = int(prob["n"])
+    nnz = int(prob["col"].shape[0])
+    p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
+    cfg = bh.TsneConfig(theta=args.theta, graph_chunk=args.chunk)
+    e = bh.embedding_from(prob["y0"])
+    shard = None
+    if world > 1:
+        from paper_2212_11506_b200.dist import Shard
+        shard = Shard(rank, world)
+    eng = bh.Engine(p, e, cfg, schedule=True, shard=shard)
+    if args.preroll:
+        eng.run(args.preroll)
+    timings = bh.StepTimings()
+    eng.run(args.warmup, timings)
+    torch.cuda.synchronize()
+    # --- timed region: K iterations, CUDA events on the launching stream
+    y_start = e.y.cpu().numpy() if rank == 0 else None
+    timings = bh.StepTimings()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record()
+        eng.run(args.steps, timings)
+        stop.record()
+        stop.synchronize()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    y_end = e.y.cpu().numpy() if rank == 0 else None
+    if rank != 0:
+        return
+    value = args.steps / (ms * 1e-3)
+    launches_per_it = eng.kernels_per_iteration()
+    stage_ms = {s: 1e3 * timings.total(s) / max(1, timings.calls(s))
+                for s in ("tree", "summarize", "attractive", "repulsive",
+                          "update", "comm")}
+
+    # --- roofline: algorithmic bytes per launch / launch time
+    counts = []
+    for ysnap in (y_start, y_end):
+        c, r = bh.compute_bounds(ysnap)
+        t = bh.summarize(bh.build_tree(bh.morton_codes(ysnap, c, r), ysnap))
+        cnt = bh.repulsive_counts(t, args.theta).astype(np.int64)
+        counts.append(cnt.sum(axis=0))
+        del t
+    cnt = np.mean(counts, axis=0)
+    # 16 B per node record visited (internal + leaf), 8 B per leaf point,
+    # 28 B per point (y_i, order, rep out, z) -- SURVEY.md 8(d)
+    rep_bytes = 16.0 * (cnt[0] + cnt[1]) + 8.0 * cnt[2] + 28.0 * n
+    att_bytes = 8.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        peak = float(json.load(open(peaks_path))["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        peak, peak_src = FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+    kernels = {}
+    for name, b in (("repulsive", rep_bytes), ("attractive", att_bytes)):
+        t_ms = stage_ms[name]
+        ach = b / (t_ms * 1e-3) / 1e9
+        kernels[name] = {"ms": t_ms, "algorithmic_bytes": b,
+                         "achieved_gbs": ach, "frac": ach / peak}
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    traffic = None
+    ncu_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(ncu_path):
+        try:
+            tr = json.load(open(ncu_path)).get(args.config, {}).get(dom)
+            traffic = None if tr is None else float(tr)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": dom,
+            "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
+            "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
+            "peak_source": peak_src,
+            "visits_per_point": (cnt[0] + cnt[1]) / n,
+            "leaf_points_per_point": cnt[2] / n}
+
+    # --- e2e through the public host-buffer API (per step: pinned host
+    #     embedding state -> device, one iteration, state -> pinned host)
+    e2e = e2e_host(bh, p, cfg, y_end, args)
+
+    # --- CPU oracle on the host cores, bounded sample from the same state
+    cpu = None
+    if args.cpu_steps > 0:
+        dt, threads, stages = cpu_oracle_time(prob, y_end, args.cpu_steps)
+        cpu = {"value": args.cpu_steps / dt, "unit": "it/s", "cores": threads,
+               "kind": "port",
+               "sample": f"{args.cpu_steps} full gradient iteration(s) of "
+                         f"{args.config} (N={n}) from the Y at the end of the "
+                         f"timed region, C/OpenMP oracle on {threads} threads "
+                         f"({cpu_model()})",
+               "stage_s": stages}
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (BASELINE.json configs[3] generator, "
+                                "SURVEY.md 8(d)); kNN via cuBLAS in setup",
+        "config": config_dict(args, n, nnz),
+        "e2e": e2e, "gpu_launches": launches_per_it * args.steps,
+        "roofline": roof, "kernels": kernels, "stage_ms": stage_ms,
+        "clocks": clk.summary(), "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def e2e_host(bh, p, cfg, y_host, args):
+    import torch
+    n = y_host.shape[0]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hy, hv, hg = pin(y_host), pin(np.zeros_like(y_host)), pin(np.ones_like(y_host))
+    e = bh.embedding_from(y_host)
+    eng = bh.Engine(p, e, cfg, schedule=True)
+    steps = max(1, min(args.steps, args.e2e_steps))
+
+    def one():
+        e.y.copy_(hy, non_blocking=True)
+        e.v.copy_(hv, non_blocking=True)
+        e.g.copy_(hg, non_blocking=True)
+        eng.run(1)
+        hy.copy_(e.y, non_blocking=True)
+        hv.copy_(e.v, non_blocking=True)
+        hg.copy_(e.g, non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    bytes_state = 3 * n * 2 * 4
+    return {"value": steps / dt, "unit": "it/s",
+            "h2d_bytes_per_step": bytes_state, "d2h_bytes_per_step": bytes_state,
+            "api": "Engine.run(1) per step on host-resident (y, v, g): pinned "
+                   "H2D, one graph-free iteration incl. bounds/centering, "
+                   "D2H; host wall clock", "steps": steps}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--preroll", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c0", "c1", "c2", "c3"])
+    ap.add_argument("--theta", type=float, default=0.5)
+    ap.add_argument("--chunk", type=int, default=25)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--ref-max-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        if args.impl == "reference":
+            reference_arm(args, rank, world)
+        else:
+            ours_arm(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

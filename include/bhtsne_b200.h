@@ -53,13 +53,13 @@ typedef void *bh_stream_t; /* cudaStream_t */
  * re-centering (optimizer.py:220-221) that bh_morton applies when asked;
  * bounds already describe the re-centred points.  nonfinite: set to 1 when a
  * coordinate was NaN/Inf (quadtree.py:143-144). */
-typedef struct bh_bounds {
+typedef struct bh_bounds_t {
     double c0, c1, r_span;
     double root0, root1, scale;
     float shift0, shift1;
     int32_t nonfinite;
     int32_t code_bits;
-} bh_bounds;
+} bh_bounds_t;
 
 /* Optimiser schedule, resident on the device so that whole iterations can be
  * captured in one CUDA graph.  Mirrors TsneConfig (optimizer.py:43-57) and
@@ -68,7 +68,7 @@ typedef struct bh_bounds {
  * momentum_switch (MOMENTUM_SWITCH_ITER = 250, optimizer.py:40).
  * `bad` = (iteration << 32 | point) of the first non-finite gradient
  * (optimizer.py:208-211), INT64_MAX while none; `z` = the last Z. */
-typedef struct bh_sched {
+typedef struct bh_sched_t {
     int32_t iteration;
     int32_t exaggeration_iters;
     int32_t momentum_switch;
@@ -79,7 +79,7 @@ typedef struct bh_sched {
     float pad1;
     int64_t bad;
     double z;
-} bh_sched;
+} bh_sched_t;
 
 /* Node record of the level-contiguous quadtree (16 bytes):
  *   x, y  : centre of mass (float32, quadtree.py:488-508)
@@ -95,7 +95,7 @@ typedef struct bh_sched {
 /* Quadtree arrays (caller-allocated; capacity = n * (max_depth + 1) + 1 is
  * always sufficient, bh_tree_node_bound()).  Replaces MortonQuadtree
  * (quadtree.py:66-85). */
-typedef struct bh_tree {
+typedef struct bh_tree_t {
     int64_t n_points;
     int64_t node_capacity;
     int32_t code_bits; /* 32 or 64 */
@@ -113,7 +113,8 @@ typedef struct bh_tree {
     float *ys;           /* 2n: coordinates in sorted order (quadtree.py:476) */
     int32_t *pt_leaf;    /* n: the leaf whose first point is t, else -1 */
     int32_t *status;     /* device int32: BH_OK or BH_ERR_CAPACITY after build */
-} bh_tree;
+    int32_t *rank;       /* optional n: rank[order[t]] = t (NULL: skipped) */
+} bh_tree_t;
 
 const char *bh_last_error(void);
 int bh_abi_version(void);
@@ -122,11 +123,11 @@ int64_t bh_tree_node_bound(int64_t n, int code_bits);
 /* ---- bounds + Morton codes: compute_bounds / morton_codes --------------
  * quadtree.py:133-153, 177-185, 230-242. */
 size_t bh_bounds_workspace_bytes(int64_t n);
-int bh_bounds(const float *y, int64_t n, int code_bits, bh_bounds *out,
+int bh_bounds(const float *y, int64_t n, int code_bits, bh_bounds_t *out,
               void *ws, size_t ws_bytes, bh_stream_t stream);
 /* codes[i] for point i; apply_shift: first re-centre y in place by
  * (shift0, shift1) (the fused update/centering of gradient_step). */
-int bh_morton(float *y, int64_t n, const bh_bounds *bounds, int code_bits,
+int bh_morton(float *y, int64_t n, const bh_bounds_t *bounds, int code_bits,
               int apply_shift, void *codes, bh_stream_t stream);
 
 /* ---- stable radix sort: _radix_argsort (quadtree.py:188-227) ------------
@@ -147,13 +148,13 @@ int bh_sort_pairs(const void *keys, const uint32_t *vals, int64_t n,
  * ys = y[order].  On overflow of node_capacity, *tree->status is set to
  * BH_ERR_CAPACITY and the tree is left incomplete. */
 size_t bh_tree_workspace_bytes(int64_t n, int code_bits);
-int bh_build_tree(const bh_tree *tree, const float *y, void *ws,
+int bh_build_tree(const bh_tree_t *tree, const float *y, void *ws,
                   size_t ws_bytes, bh_stream_t stream);
 
 /* ---- summarize (quadtree.py:481-519) --------------------------------------
  * Bottom-up centre of mass and count; bit-identical to the reference
  * (f64 sums in reference order, stored as float32). */
-int bh_summarize(const bh_tree *tree, bh_stream_t stream);
+int bh_summarize(const bh_tree_t *tree, bh_stream_t stream);
 
 /* ---- attractive force (forces.py:56-82) ---------------------------------
  * attr[i] = sum_t v_t*(y_i - y_j)/(1+|y_i-y_j|^2) over CSR row i, for rows
@@ -164,21 +165,30 @@ int bh_summarize(const bh_tree *tree, bh_stream_t stream);
 int bh_attractive(const int64_t *row_ptr, const int32_t *col,
                   const float *val, int64_t n_rows, int padded,
                   const float *y, int64_t row_begin, int64_t row_end,
-                  float exaggeration, const bh_sched *sched, float *attr,
+                  float exaggeration, const bh_sched_t *sched, float *attr,
                   bh_stream_t stream);
 
 /* ---- repulsive Barnes-Hut force (forces.py:85-150) -----------------------
  * Warp-synchronous traversal over sorted positions [t_begin, t_end) with
  * per-lane acceptance masks (the exact per-point BH semantics of the
- * reference).  Writes rep[id] (float32 pairs, by point id), zpart[id]
- * (float64, optional) and the fixed-order reduction of Z over the range
- * into *z_out (optional).  `counts` (optional, 4 int32 per point id):
- * internal visits, leaf-node visits, leaf points touched, accepted. */
+ * reference).  Query coordinates: y_query[id] (by point id) or, when NULL,
+ * the tree's own ys.  Outputs indexed by point id (sorted_out = 0) or by
+ * t - t_begin (sorted_out = 1): rep (float32 pairs), zpart (float64,
+ * optional), counts (optional, 4 int32: internal visits, leaf-node visits,
+ * leaf points touched, accepted).  zblock (optional; else in ws) receives
+ * one f64 partial of Z per 256 consecutive sorted points; z_out (optional)
+ * their fixed-order sum (the same reduction bh_sum_partials applies, so Z
+ * does not depend on how ranges are split across GPUs). */
 size_t bh_repulsive_workspace_bytes(int64_t n);
-int bh_repulsive(const bh_tree *tree, const bh_bounds *bounds, double theta,
-                 int64_t t_begin, int64_t t_end, float *rep, double *zpart,
-                 double *z_out, int32_t *counts, void *ws, size_t ws_bytes,
-                 bh_stream_t stream);
+int bh_repulsive(const bh_tree_t *tree, const bh_bounds_t *bounds,
+                 double theta, const float *y_query, int64_t t_begin,
+                 int64_t t_end, int sorted_out, float *rep, double *zpart,
+                 double *zblock, double *z_out, int32_t *counts, void *ws,
+                 size_t ws_bytes, bh_stream_t stream);
+/* *out = fixed-order sum of n per-CTA Z partials (see bh_repulsive). */
+int bh_sum_partials(const double *x, int64_t n, double *out,
+                    bh_stream_t stream);
+#define BH_REP_POINTS_PER_PARTIAL 256
 
 /* ---- exact O(N^2) repulsion (forces.py:153-182) -------------------------- */
 size_t bh_repulsive_exact_workspace_bytes(int64_t n);
@@ -198,13 +208,16 @@ int bh_kl_rows(const int64_t *row_ptr, const int32_t *col, const float *val,
  * the new y is computed (f64) and published, with the bounds of the
  * re-centred points, into *bounds_out (shift0/shift1 = the f32 mean).  The
  * re-centering itself is applied by bh_center or by the next bh_morton
- * (apply_shift=1).  Increments sched->iteration. */
+ * (apply_shift=1).  rep is read at rep_rank[i] when rep_rank is not NULL
+ * (sorted-order forces of the multi-GPU path), else at i.  Z is sched->z.
+ * Increments sched->iteration. */
 size_t bh_update_workspace_bytes(int64_t n);
 int bh_update(float *y, float *v, float *g, const float *attr,
-              const float *rep, int64_t n, bh_sched *sched,
-              bh_bounds *bounds_out, int code_bits, void *ws, size_t ws_bytes,
+              const float *rep, const int32_t *rep_rank, int64_t n,
+              bh_sched_t *sched,
+              bh_bounds_t *bounds_out, int code_bits, void *ws, size_t ws_bytes,
               bh_stream_t stream);
-int bh_center(float *y, int64_t n, const bh_bounds *bounds,
+int bh_center(float *y, int64_t n, const bh_bounds_t *bounds,
               bh_stream_t stream);
 
 /* ---- binary-search perplexity: calibrate_perplexity (affinity.py:61-118) --
@@ -217,14 +230,16 @@ int bh_bsp(const float *sqd, int64_t n, int64_t k, double perplexity,
  * p_ij = max((p_j|i + p_i|j) / 2N, eps64) as float32 CSR with ascending
  * columns.  Two calls: bh_symmetrize_plan sorts the 2NK directed entries and
  * writes the nnz to *nnz_out (device int64); after the caller allocates the
- * outputs, bh_symmetrize_fill writes row_ptr (n+1), col and val (nnz). */
+ * outputs, bh_symmetrize_fill (same workspace, nnz from the plan) writes
+ * row_ptr (n+1), col and val (nnz). */
 size_t bh_symmetrize_workspace_bytes(int64_t n, int64_t k);
 int bh_symmetrize_plan(const int64_t *indices, int64_t n, int64_t k,
                        int64_t *nnz_out, void *ws, size_t ws_bytes,
                        bh_stream_t stream);
 int bh_symmetrize_fill(const double *cond, int64_t n, int64_t k,
-                       int64_t *row_ptr, int32_t *col, float *val, void *ws,
-                       size_t ws_bytes, bh_stream_t stream);
+                       const int64_t *nnz, int64_t *row_ptr, int32_t *col,
+                       float *val, void *ws, size_t ws_bytes,
+                       bh_stream_t stream);
 /* Pads a CSR so every row starts at a multiple of 4 entries (pad entries:
  * col = row, val = 0).  out_row_ptr has n+1 entries; out capacity from
  * bh_pad_csr_size (device int64 result in *padded_nnz). */
@@ -235,6 +250,13 @@ int bh_pad_csr_size(const int64_t *row_ptr, int64_t n, int64_t *out_row_ptr,
 int bh_pad_csr_fill(const int64_t *row_ptr, const int32_t *col,
                     const float *val, int64_t n, const int64_t *out_row_ptr,
                     int32_t *out_col, float *out_val, bh_stream_t stream);
+
+/* ---- exact kNN (knn.py:36-73) ---------------------
+ * f64 squared distances summed over columns in order, k smallest per row,
+ * ties -> lower id, self excluded; distances returned as float32.
+ * x: (n, d) float32 row-major, d <= 64, k <= 128. */
+int bh_knn(const float *x, int64_t n, int64_t d, int64_t k, int64_t *out_idx,
+           float *out_sqd, bh_stream_t stream);
 
 #ifdef __cplusplus
 }

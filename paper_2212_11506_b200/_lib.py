@@ -1,0 +1,172 @@
+"""ctypes binding of libbhtsne_b200.so (include/bhtsne_b200.h).
+
+The library is the only compute path: there is no CPU fallback.  Loading
+fails loudly when the shared object is missing or no CUDA device is present.
+torch supplies device memory and streams; no torch type crosses the ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbhtsne_b200.so")
+
+_lib = None
+
+BH_LEAF_BIT = 0x80000000
+BH_CHILD_MASK = 0x1FFFFFFF
+BH_NKIDS_SHIFT = 29
+BH_ERR_CAPACITY = -3
+
+# device-resident structs, viewed through numpy structured dtypes
+BOUNDS_DTYPE = np.dtype([
+    ("c0", "f8"), ("c1", "f8"), ("r_span", "f8"), ("root0", "f8"),
+    ("root1", "f8"), ("scale", "f8"), ("shift0", "f4"), ("shift1", "f4"),
+    ("nonfinite", "i4"), ("code_bits", "i4")])
+SCHED_DTYPE = np.dtype([
+    ("iteration", "i4"), ("exaggeration_iters", "i4"),
+    ("momentum_switch", "i4"), ("pad0", "i4"), ("exaggeration", "f4"),
+    ("momentum_early", "f4"), ("momentum_late", "f4"),
+    ("learning_rate", "f4"), ("min_gain", "f4"), ("pad1", "f4"),
+    ("bad", "i8"), ("z", "f8")])
+assert BOUNDS_DTYPE.itemsize == 64 and SCHED_DTYPE.itemsize == 56
+INT64_MAX = np.iinfo(np.int64).max
+
+
+class TreeStruct(C.Structure):
+    """bh_tree_t: host struct of device pointers."""
+
+    _fields_ = [
+        ("n_points", C.c_int64), ("node_capacity", C.c_int64),
+        ("code_bits", C.c_int32), ("max_depth", C.c_int32),
+        ("node", C.c_void_p), ("parent", C.c_void_p),
+        ("node_start", C.c_void_p), ("leaf_end", C.c_void_p),
+        ("nkids", C.c_void_p), ("arrive", C.c_void_p),
+        ("level_off", C.c_void_p), ("order", C.c_void_p),
+        ("sorted_codes", C.c_void_p), ("ys", C.c_void_p),
+        ("pt_leaf", C.c_void_p), ("status", C.c_void_p),
+        ("rank", C.c_void_p),
+    ]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_SZ = C.c_size_t
+
+SIGNATURES = {
+    "bh_last_error": ([], C.c_char_p),
+    "bh_abi_version": ([], C.c_int),
+    "bh_tree_node_bound": ([_I64, C.c_int], _I64),
+    "bh_bounds_workspace_bytes": ([_I64], _SZ),
+    "bh_bounds": ([_P, _I64, C.c_int, _P, _P, _SZ, _P], C.c_int),
+    "bh_morton": ([_P, _I64, _P, C.c_int, C.c_int, _P, _P], C.c_int),
+    "bh_sort_workspace_bytes": ([_I64, C.c_int], _SZ),
+    "bh_sort": ([_P, _I64, C.c_int, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_sort_pairs": ([_P, _P, _I64, C.c_int, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_tree_workspace_bytes": ([_I64, C.c_int], _SZ),
+    "bh_build_tree": ([C.POINTER(TreeStruct), _P, _P, _SZ, _P], C.c_int),
+    "bh_summarize": ([C.POINTER(TreeStruct), _P], C.c_int),
+    "bh_attractive": ([_P, _P, _P, _I64, C.c_int, _P, _I64, _I64, C.c_float,
+                       _P, _P, _P], C.c_int),
+    "bh_repulsive_workspace_bytes": ([_I64], _SZ),
+    "bh_repulsive": ([C.POINTER(TreeStruct), _P, C.c_double, _P, _I64, _I64,
+                      C.c_int, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_sum_partials": ([_P, _I64, _P, _P], C.c_int),
+    "bh_repulsive_exact_workspace_bytes": ([_I64], _SZ),
+    "bh_repulsive_exact": ([_P, _I64, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_kl_workspace_bytes": ([_I64], _SZ),
+    "bh_kl_rows": ([_P, _P, _P, _I64, C.c_int, _P, _P, _P, _P, _SZ, _P],
+                   C.c_int),
+    "bh_update_workspace_bytes": ([_I64], _SZ),
+    "bh_update": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P, C.c_int, _P, _SZ,
+                   _P], C.c_int),
+    "bh_center": ([_P, _I64, _P, _P], C.c_int),
+    "bh_bsp": ([_P, _I64, _I64, C.c_double, C.c_double, _I64, _P, _P, _P],
+               C.c_int),
+    "bh_symmetrize_workspace_bytes": ([_I64, _I64], _SZ),
+    "bh_symmetrize_plan": ([_P, _I64, _I64, _P, _P, _SZ, _P], C.c_int),
+    "bh_symmetrize_fill": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P],
+                           C.c_int),
+    "bh_pad_csr_workspace_bytes": ([_I64], _SZ),
+    "bh_pad_csr_size": ([_P, _I64, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_pad_csr_fill": ([_P, _P, _P, _I64, _P, _P, _P, _P], C.c_int),
+    "bh_knn": ([_P, _I64, _I64, _I64, _P, _P, _P], C.c_int),
+}
+
+
+def load(require_device: bool = True):
+    """Load the CUDA library (raises if it is missing; no fallback)."""
+    global _lib
+    if require_device and not torch.cuda.is_available():
+        raise RuntimeError("paper_2212_11506_b200 needs a CUDA device (B200, "
+                           "sm_100a); there is no CPU fallback")
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (args, res) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.bh_abi_version() != 1:
+        raise RuntimeError("libbhtsne_b200 ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def load_symbols_only():
+    """Load without requiring a device (used by the CPU ABI tests)."""
+    return load(require_device=False)
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = _lib.bh_last_error().decode(errors="replace") if _lib else ""
+        if rc == -1:
+            raise ValueError(msg or what)
+        raise RuntimeError(f"{what}: {msg} (code {rc})")
+
+
+def call(name: str, *args):
+    lib = load()
+    check(getattr(lib, name)(*args), name)
+
+
+def ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def device() -> torch.device:
+    load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    """Zero-filled scratch (the library leaves its counters at zero)."""
+    return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8,
+                       device=device())
+
+
+def struct_tensor(dtype: np.dtype, values: dict | None = None) -> torch.Tensor:
+    host = np.zeros(1, dtype)
+    for k, v in (values or {}).items():
+        host[k] = v
+    t = torch.from_numpy(host.view(np.uint8).copy())
+    return t.to(device())
+
+
+def read_struct(t: torch.Tensor, dtype: np.dtype):
+    return t.cpu().numpy().view(dtype)[0]

@@ -1,0 +1,516 @@
+// Force kernels: Barnes-Hut repulsion (forces.py:85-150), attractive CSR
+// sweep (forces.py:56-82), exact O(N^2) repulsion (forces.py:153-182) and
+// the KL rows (optimizer.py:227-239).
+#include "common.cuh"
+
+namespace bh {
+
+// ---------------------------------------------------------------------------
+// Repulsion: warp-synchronous BH traversal with per-lane acceptance masks.
+//
+// A warp owns 32 consecutive points in Morton order.  Its stack holds child
+// GROUPS (the consecutive children of one opened node) plus the mask of
+// lanes that opened that node.  Popping a group loads its <= 4 node records
+// once for the whole warp (a broadcast of <= 64 contiguous bytes); every lane
+// in the mask applies the reference's per-point rule to each child exactly
+// as forces.py:99-128 does -- a leaf contributes its points directly (self
+// skipped by index), an internal node is accepted iff (2r)^2 < theta^2 d^2,
+// else that lane needs its children.  The children are pushed once with the
+// ballot of the lanes that need them.  Each lane therefore visits exactly the
+// node set of its own reference traversal (same accept decisions, same
+// contributions); lanes that accepted or never reached a node idle for it.
+// Pair math is f32; contributions of one popped group are summed in f32 and
+// added to f64 accumulators.
+// ---------------------------------------------------------------------------
+constexpr int kRepWarps = 8;
+constexpr int kRepThreads = kRepWarps * 32;
+
+// Deterministic warp reduction: lane-strided sequential partials, then a
+// butterfly.  Called by one full warp; every lane returns the total.
+__device__ __forceinline__ double fixed_sum(const double *x, int64_t n) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x & 31; i < n; i += 32) s = __dadd_rn(s, __ldcg(&x[i]));
+    return warp_sum(s);
+}
+
+struct RepCounts {
+    int internal, leafnodes, leafpts, accepted;
+};
+
+template <int D, bool COUNT>
+__global__ void __launch_bounds__(kRepThreads)
+k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
+            const int32_t *__restrict__ order,
+            const float2 *__restrict__ y_query,
+            const bh_bounds_t *__restrict__ bounds,
+            const int32_t *__restrict__ status, float theta2, int64_t t_begin,
+            int64_t t_end, int sorted_out, float2 *__restrict__ rep,
+            double *__restrict__ zpart, int4 *__restrict__ counts,
+            double *__restrict__ zblock, unsigned *__restrict__ ticket,
+            double *__restrict__ z_out) {
+    constexpr int CAP = 3 * D + 2;
+    __shared__ uint32_t s_first[kRepWarps][CAP];
+    __shared__ uint32_t s_mask[kRepWarps][CAP];
+    __shared__ uint8_t s_meta[kRepWarps][CAP];
+    __shared__ float s_side2[D + 1];
+    __shared__ double s_z[kRepWarps];
+    __shared__ bool s_last;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x <= D) {
+        // cell side at depth d: 2 * r_span / 2^d (radius halves exactly)
+        double side = ldexp(2.0 * bounds->r_span, -(int)threadIdx.x);
+        s_side2[threadIdx.x] = (float)(side * side);
+    }
+    __syncthreads();
+
+    const int64_t t = t_begin + ((int64_t)blockIdx.x * kRepWarps + warp) * 32 + lane;
+    const bool valid = t < t_end && *status == BH_OK;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    float2 yi = make_float2(0.f, 0.f);
+    if (valid) yi = y_query ? y_query[order[t]] : ys[t];
+    const uint32_t self = (uint32_t)t;
+    double r0 = 0.0, r1 = 0.0, z = 0.0;
+    RepCounts cn = {0, 0, 0, 0};
+
+    int sp = 0;
+    if (act) {
+        if (lane == 0) {
+            s_first[warp][0] = 0;
+            s_mask[warp][0] = act;
+            s_meta[warp][0] = 0;  // (count-1) | depth << 2
+        }
+        sp = 1;
+        __syncwarp();
+    }
+    while (sp > 0) {
+        --sp;
+        const uint32_t first = s_first[warp][sp];
+        const uint32_t mask = s_mask[warp][sp];
+        const uint32_t meta = s_meta[warp][sp];
+        __syncwarp();
+        const int cnt = (int)(meta & 3u) + 1;
+        const int depth = (int)(meta >> 2);
+        const bool mine = (mask >> lane) & 1u;
+        const float side2 = s_side2[depth];
+        float fz = 0.f, fx = 0.f, fy = 0.f;
+        uint32_t push_mask[4], push_info[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            push_mask[c] = 0;
+            push_info[c] = 0;
+            if (c < cnt) {
+                const float4 rec = __ldg(&node[first + c]);
+                const uint32_t info = __float_as_uint(rec.w);
+                const uint32_t m = __float_as_uint(rec.z);
+                if (info & BH_LEAF_BIT) {
+                    const uint32_t s = info & ~BH_LEAF_BIT;
+                    if (COUNT && mine) {
+                        cn.leafnodes++;
+                        cn.leafpts += (int)m;
+                    }
+                    if (m == 1) {
+                        // single-point leaf: its com is the point itself
+                        if (mine && s != self) {
+                            float dx = yi.x - rec.x, dy = yi.y - rec.y;
+                            float k = __frcp_rn(1.0f + dx * dx + dy * dy);
+                            float k2 = k * k;
+                            fz += k;
+                            fx += k2 * dx;
+                            fy += k2 * dy;
+                        }
+                    } else {
+                        // coincident-code bucket at max depth: warp-cooperative
+                        for (uint32_t b = 0; b < m; b += 32) {
+                            const uint32_t q = s + b + lane;
+                            float2 pq = (b + lane < m) ? ys[q] : make_float2(0.f, 0.f);
+                            const int nb = (int)min(32u, m - b);
+                            float bz = 0.f, bx = 0.f, by = 0.f;
+                            for (int jj = 0; jj < nb; jj++) {
+                                float px = __shfl_sync(0xffffffffu, pq.x, jj);
+                                float py = __shfl_sync(0xffffffffu, pq.y, jj);
+                                if (mine && s + b + jj != self) {
+                                    float dx = yi.x - px, dy = yi.y - py;
+                                    float k = __frcp_rn(1.0f + dx * dx + dy * dy);
+                                    float k2 = k * k;
+                                    bz += k;
+                                    bx += k2 * dx;
+                                    by += k2 * dy;
+                                }
+                            }
+                            z += (double)bz;
+                            r0 += (double)bx;
+                            r1 += (double)by;
+                        }
+                    }
+                } else {
+                    float dx = yi.x - rec.x, dy = yi.y - rec.y;
+                    float d2 = dx * dx + dy * dy;
+                    bool acc = side2 < theta2 * d2;
+                    if (COUNT && mine) {
+                        cn.internal++;
+                        cn.accepted += acc;
+                    }
+                    if (mine && acc) {
+                        float k = __frcp_rn(1.0f + d2);
+                        float mk = (float)m * k;
+                        float mk2 = mk * k;
+                        fz += mk;
+                        fx += mk2 * dx;
+                        fy += mk2 * dy;
+                    }
+                    push_mask[c] = __ballot_sync(0xffffffffu, mine && !acc);
+                    push_info[c] = info;
+                }
+            }
+        }
+        z += (double)fz;
+        r0 += (double)fx;
+        r1 += (double)fy;
+        // push groups in reverse so the first child is opened first
+#pragma unroll
+        for (int c = 3; c >= 0; c--) {
+            if (push_mask[c]) {
+                if (lane == 0) {
+                    s_first[warp][sp] = push_info[c] & BH_CHILD_MASK;
+                    s_mask[warp][sp] = push_mask[c];
+                    s_meta[warp][sp] = (uint8_t)(((push_info[c] >> BH_NKIDS_SHIFT) & 3u) |
+                                                 ((uint32_t)(depth + 1) << 2));
+                }
+                sp++;
+            }
+        }
+        __syncwarp();
+    }
+
+    if (valid) {
+        const int64_t o = sorted_out ? t - t_begin : (int64_t)order[t];
+        rep[o] = make_float2((float)r0, (float)r1);
+        if (zpart) zpart[o] = z;
+        if (COUNT) counts[o] = make_int4(cn.internal, cn.leafnodes, cn.leafpts, cn.accepted);
+    }
+    // Z: per-CTA partial (256 points in Morton order), then one fixed-order
+    // warp reduction over all CTA partials (fixed_sum) -- the same
+    // reduction the multi-GPU path applies to the gathered partials, so Z is
+    // bitwise independent of the GPU count.
+    double wz = warp_sum(z);
+    if (lane == 0) s_z[warp] = wz;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bz = 0.0;
+        for (int w = 0; w < kRepWarps; w++) bz = __dadd_rn(bz, s_z[w]);
+        zblock[blockIdx.x] = bz;
+        if (z_out) {
+            __threadfence();
+            s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        }
+    }
+    if (!z_out) return;
+    __syncthreads();
+    if (s_last && warp == 0) {
+        __threadfence();
+        double tot = fixed_sum(zblock, gridDim.x);
+        if (lane == 0) {
+            *z_out = tot;
+            *ticket = 0;
+        }
+    }
+}
+
+// Sum of gathered per-CTA Z partials into *out (one warp, fixed order).
+__global__ void k_fixed_sum(const double *__restrict__ x, int64_t n,
+                            double *__restrict__ out) {
+    double s = fixed_sum(x, n);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// ---------------------------------------------------------------------------
+// Attractive CSR sweep: a group of G lanes per row; padded rows start at a
+// multiple of 4 entries so each lane issues 128-bit loads of 4 column ids
+// and 4 values (pad entries have value 0 and contribute exactly 0).
+// ---------------------------------------------------------------------------
+template <int G, bool PADDED>
+__global__ void __launch_bounds__(256)
+k_attractive(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+             const float *__restrict__ val, const float2 *__restrict__ y,
+             int64_t row_begin, int64_t row_end, float exag_param,
+             const bh_sched_t *__restrict__ sched, float2 *__restrict__ attr) {
+    const float exag = sched ? (sched->iteration < sched->exaggeration_iters
+                                    ? sched->exaggeration
+                                    : 1.0f)
+                             : exag_param;
+    const int gl = threadIdx.x % G;
+    const int64_t row = row_begin + (int64_t)blockIdx.x * (256 / G) + threadIdx.x / G;
+    const bool ok = row < row_end;
+    int64_t s = 0, e = 0;
+    float2 yi = make_float2(0.f, 0.f);
+    if (ok) {
+        s = rp[row];
+        e = rp[row + 1];
+        yi = y[row];
+    }
+    double a0 = 0.0, a1 = 0.0;
+    if (PADDED) {
+        for (int64_t q = s + 4 * gl; q < e; q += 4 * G) {
+            const int4 c = __ldcs(reinterpret_cast<const int4 *>(col + q));
+            const float4 v = __ldcs(reinterpret_cast<const float4 *>(val + q));
+            const float2 y0 = __ldg(&y[c.x]), y1 = __ldg(&y[c.y]);
+            const float2 y2 = __ldg(&y[c.z]), y3 = __ldg(&y[c.w]);
+            float fx = 0.f, fy = 0.f;
+#define BH_ATTR_TERM(YJ, V)                                                   \
+    {                                                                         \
+        float dx = yi.x - YJ.x, dy = yi.y - YJ.y;                             \
+        float pq = __fmul_rn(V, exag) * __frcp_rn(1.0f + dx * dx + dy * dy);  \
+        fx += pq * dx;                                                        \
+        fy += pq * dy;                                                        \
+    }
+            BH_ATTR_TERM(y0, v.x)
+            BH_ATTR_TERM(y1, v.y)
+            BH_ATTR_TERM(y2, v.z)
+            BH_ATTR_TERM(y3, v.w)
+            a0 += (double)fx;
+            a1 += (double)fy;
+        }
+    } else {
+        for (int64_t q = s + gl; q < e; q += G) {
+            const int32_t c = col[q];
+            const float v = val[q];
+            const float2 yj = __ldg(&y[c]);
+            float fx = 0.f, fy = 0.f;
+            BH_ATTR_TERM(yj, v)
+            a0 += (double)fx;
+            a1 += (double)fy;
+        }
+    }
+#undef BH_ATTR_TERM
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (ok && gl == 0) attr[row] = make_float2((float)a0, (float)a1);
+}
+
+// ---------------------------------------------------------------------------
+// Exact O(N^2) repulsion (forces.py:153-173): the end-of-run KL needs the
+// exact Z.  Tiles of points staged in shared memory; f32 pair math, f32
+// partial per tile, f64 accumulation.
+// ---------------------------------------------------------------------------
+constexpr int kExTile = 1024;
+
+__global__ void __launch_bounds__(256)
+k_repulsive_exact(const float2 *__restrict__ y, int64_t n,
+                  float2 *__restrict__ rep, double *__restrict__ zpart,
+                  double *__restrict__ zblock, unsigned *__restrict__ ticket,
+                  double *__restrict__ z_out) {
+    __shared__ float2 s_y[kExTile];
+    __shared__ double s_z[8];
+    __shared__ bool s_last;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool ok = i < n;
+    const float2 yi = ok ? y[i] : make_float2(0.f, 0.f);
+    double z = 0.0, r0 = 0.0, r1 = 0.0;
+    for (int64_t j0 = 0; j0 < n; j0 += kExTile) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < kExTile; q += blockDim.x)
+            s_y[q] = j0 + q < n ? y[j0 + q] : make_float2(0.f, 0.f);
+        __syncthreads();
+        const int nb = (n - j0) < kExTile ? (int)(n - j0) : kExTile;
+        float fz = 0.f, fx = 0.f, fy = 0.f;
+        for (int q = 0; q < nb; q++) {
+            const float2 p = s_y[q];
+            float dx = yi.x - p.x, dy = yi.y - p.y;
+            float k = __frcp_rn(1.0f + dx * dx + dy * dy);
+            if (j0 + q == i) k = 0.f;
+            float k2 = k * k;
+            fz += k;
+            fx += k2 * dx;
+            fy += k2 * dy;
+        }
+        z += (double)fz;
+        r0 += (double)fx;
+        r1 += (double)fy;
+    }
+    if (ok) {
+        if (rep) rep[i] = make_float2((float)r0, (float)r1);
+        if (zpart) zpart[i] = z;
+    }
+    double wz = warp_sum(ok ? z : 0.0);
+    if ((threadIdx.x & 31) == 0) s_z[threadIdx.x >> 5] = wz;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bz = 0.0;
+        for (int w = 0; w < 8; w++) bz += s_z[w];
+        zblock[blockIdx.x] = bz;
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        double tot = 0.0;
+        for (unsigned b = 0; b < gridDim.x; b++) tot += __ldcg(&zblock[b]);
+        *z_out = tot;
+        *ticket = 0;
+    }
+}
+
+// KL rows (optimizer.py:227-239) in f64, one warp per row.
+__global__ void __launch_bounds__(256)
+k_kl_rows(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+          const float *__restrict__ val, int64_t n, const float2 *__restrict__ y,
+          const double *__restrict__ zp, double *__restrict__ part,
+          unsigned *__restrict__ ticket, double *__restrict__ kl_out) {
+    __shared__ double s_a[8];
+    __shared__ bool s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double Z = *zp;
+    double acc = 0.0;
+    for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < n;
+         row += (int64_t)gridDim.x * 8) {
+        const float2 yi = y[row];
+        for (int64_t q = rp[row] + lane; q < rp[row + 1]; q += 32) {
+            const float p = val[q];
+            if (p == 0.0f) continue;  // padding
+            const float2 yj = y[col[q]];
+            double dx = (double)yi.x - (double)yj.x;
+            double dy = (double)yi.y - (double)yj.y;
+            double pd = (double)p;
+            acc += pd * log(pd * Z * (1.0 + dx * dx + dy * dy));
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_a[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < 8; w++) b += s_a[w];
+        part[blockIdx.x] = b;
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        double tot = 0.0;
+        for (unsigned b = 0; b < gridDim.x; b++) tot += __ldcg(&part[b]);
+        *kl_out = tot;
+        *ticket = 0;
+    }
+}
+
+static int rep_grid(int64_t npts) { return bh_blocks(npts, kRepThreads); }
+
+}  // namespace bh
+
+using namespace bh;
+
+extern "C" size_t bh_repulsive_workspace_bytes(int64_t n) {
+    return bh_align(sizeof(double) * rep_grid(n)) + 256;
+}
+
+extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
+                            double theta, const float *y_query,
+                            int64_t t_begin, int64_t t_end, int sorted_out,
+                            float *rep, double *zpart, double *zblock,
+                            double *z_out, int32_t *counts, void *ws,
+                            size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(theta >= 0, "theta must be >= 0, got %g", theta);
+    BH_REQUIRE(t_begin >= 0 && t_end <= t->n_points && t_begin <= t_end,
+               "bad point range");
+    if (t_end == t_begin) return BH_OK;
+    const int grid = rep_grid(t_end - t_begin);
+    BH_REQUIRE(ws_bytes >= bh_repulsive_workspace_bytes(t_end - t_begin),
+               "repulsive workspace too small");
+    char *w = (char *)ws;
+    if (!zblock) zblock = (double *)w;
+    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(double) * grid));
+    const float theta2 = (float)(theta * theta);
+    cudaStream_t st = bh_cs(stream);
+#define BH_REP_LAUNCH(D, CNT)                                                 \
+    k_repulsive<D, CNT><<<grid, kRepThreads, 0, st>>>(                        \
+        (const float4 *)t->node, (const float2 *)t->ys, t->order,             \
+        (const float2 *)y_query, bounds, t->status, theta2, t_begin, t_end,   \
+        sorted_out, (float2 *)rep, zpart, (int4 *)counts, zblock, ticket,     \
+        z_out)
+    if (t->code_bits == 32) {
+        if (counts) BH_REP_LAUNCH(16, true); else BH_REP_LAUNCH(16, false);
+    } else if (t->code_bits == 64) {
+        if (counts) BH_REP_LAUNCH(32, true); else BH_REP_LAUNCH(32, false);
+    } else {
+        return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
+    }
+#undef BH_REP_LAUNCH
+    BH_CHECK_LAUNCH("k_repulsive");
+    return BH_OK;
+}
+
+extern "C" int bh_sum_partials(const double *x, int64_t n, double *out,
+                               bh_stream_t stream) {
+    k_fixed_sum<<<1, 32, 0, bh_cs(stream)>>>(x, n, out);
+    BH_CHECK_LAUNCH("k_fixed_sum");
+    return BH_OK;
+}
+
+extern "C" int bh_attractive(const int64_t *row_ptr, const int32_t *col,
+                             const float *val, int64_t n_rows, int padded,
+                             const float *y, int64_t row_begin,
+                             int64_t row_end, float exaggeration,
+                             const bh_sched_t *sched, float *attr,
+                             bh_stream_t stream) {
+    BH_REQUIRE(row_begin >= 0 && row_end <= n_rows && row_begin <= row_end,
+               "bad row range");
+    if (row_end == row_begin) return BH_OK;
+    constexpr int G = 8;
+    const int grid = bh_blocks(row_end - row_begin, 256 / G);
+    cudaStream_t st = bh_cs(stream);
+    if (padded)
+        k_attractive<G, true><<<grid, 256, 0, st>>>(
+            row_ptr, col, val, (const float2 *)y, row_begin, row_end,
+            exaggeration, sched, (float2 *)attr);
+    else
+        k_attractive<G, false><<<grid, 256, 0, st>>>(
+            row_ptr, col, val, (const float2 *)y, row_begin, row_end,
+            exaggeration, sched, (float2 *)attr);
+    BH_CHECK_LAUNCH("k_attractive");
+    return BH_OK;
+}
+
+extern "C" size_t bh_repulsive_exact_workspace_bytes(int64_t n) {
+    return bh_align(sizeof(double) * bh_blocks(n, 256)) + 256;
+}
+
+extern "C" int bh_repulsive_exact(const float *y, int64_t n, float *rep,
+                                  double *zpart, double *z_out, void *ws,
+                                  size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(n >= 2, "need at least 2 points");
+    BH_REQUIRE(ws_bytes >= bh_repulsive_exact_workspace_bytes(n),
+               "exact workspace too small");
+    const int grid = bh_blocks(n, 256);
+    char *w = (char *)ws;
+    k_repulsive_exact<<<grid, 256, 0, bh_cs(stream)>>>(
+        (const float2 *)y, n, (float2 *)rep, zpart, (double *)w,
+        (unsigned *)(w + bh_align(sizeof(double) * grid)), z_out);
+    BH_CHECK_LAUNCH("k_repulsive_exact");
+    return BH_OK;
+}
+
+extern "C" size_t bh_kl_workspace_bytes(int64_t n) {
+    return bh_align(sizeof(double) * kSMs * 8) + 256;
+}
+
+extern "C" int bh_kl_rows(const int64_t *row_ptr, const int32_t *col,
+                          const float *val, int64_t n, int padded,
+                          const float *y, const double *z, double *kl_out,
+                          void *ws, size_t ws_bytes, bh_stream_t stream) {
+    (void)padded;  // pad entries carry p == 0 and are skipped
+    BH_REQUIRE(ws_bytes >= bh_kl_workspace_bytes(n), "kl workspace too small");
+    int grid = bh_blocks(n, 8);
+    if (grid > kSMs * 8) grid = kSMs * 8;
+    char *w = (char *)ws;
+    k_kl_rows<<<grid, 256, 0, bh_cs(stream)>>>(
+        row_ptr, col, val, n, (const float2 *)y, z, (double *)w,
+        (unsigned *)(w + bh_align(sizeof(double) * kSMs * 8)), kl_out);
+    BH_CHECK_LAUNCH("k_kl_rows");
+    return BH_OK;
+}

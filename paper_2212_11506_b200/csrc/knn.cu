@@ -1,0 +1,103 @@
+// Exact k-nearest neighbours -- the GPU version of
+// knn_exact (knn.py:36-73) with the reference's exact semantics: squared
+// distances accumulated in f64 over the columns in order (no FMA), k
+// smallest kept by strict-less insertion over ascending candidate ids (ties
+// -> lower id), self excluded, distances stored as float32.
+//
+// One thread per query, its row held in registers as f64; candidate rows are
+// staged per CTA in shared memory (f64, broadcast reads).  The partial sum
+// is monotone, so a candidate is abandoned as soon as it exceeds the current
+// k-th distance.  The per-query top-k lives in thread-local memory.
+#include "common.cuh"
+
+namespace bh {
+
+constexpr int kKnnThreads = 128;
+constexpr int kKnnTile = 32;
+constexpr int kKnnMaxK = 128;
+
+template <int DMAX>
+__global__ void __launch_bounds__(kKnnThreads)
+k_knn(const float *__restrict__ x, int64_t n, int d, int k,
+      int64_t *__restrict__ out_idx, float *__restrict__ out_sqd) {
+    __shared__ double s_c[kKnnTile][DMAX];
+    const int64_t i = blockIdx.x * (int64_t)kKnnThreads + threadIdx.x;
+    const bool ok = i < n;
+    double q[DMAX];
+#pragma unroll
+    for (int c = 0; c < DMAX; c++) q[c] = (ok && c < d) ? (double)x[i * d + c] : 0.0;
+    double bd[kKnnMaxK];
+    int32_t bi[kKnnMaxK];
+    for (int t = 0; t < k; t++) {
+        bd[t] = INFINITY;
+        bi[t] = -1;
+    }
+    double thr = INFINITY;
+    for (int64_t j0 = 0; j0 < n; j0 += kKnnTile) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kKnnTile * DMAX; e += kKnnThreads) {
+            int r = e / DMAX, c = e % DMAX;
+            int64_t j = j0 + r;
+            s_c[r][c] = (j < n && c < d) ? (double)x[j * d + c] : 0.0;
+        }
+        __syncthreads();
+        if (!ok) continue;
+        const int nb = (n - j0) < kKnnTile ? (int)(n - j0) : kKnnTile;
+        for (int r = 0; r < nb; r++) {
+            const int64_t j = j0 + r;
+            if (j == i) continue;
+            double acc = 0.0;
+            bool keep = true;
+#pragma unroll
+            for (int c = 0; c < DMAX; c++) {
+                if (c < d) {
+                    double diff = __dsub_rn(q[c], s_c[r][c]);
+                    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                }
+                if ((c & 7) == 7 && acc > thr) {
+                    keep = false;
+                    break;
+                }
+            }
+            if (!keep || !(acc < thr)) continue;
+            int pos = k - 1;
+            while (pos > 0 && acc < bd[pos - 1]) {
+                bd[pos] = bd[pos - 1];
+                bi[pos] = bi[pos - 1];
+                pos--;
+            }
+            bd[pos] = acc;
+            bi[pos] = (int32_t)j;
+            thr = bd[k - 1];
+        }
+    }
+    if (ok) {
+        for (int t = 0; t < k; t++) {
+            out_idx[i * k + t] = bi[t];
+            out_sqd[i * k + t] = __double2float_rn(bd[t]);
+        }
+    }
+}
+
+}  // namespace bh
+
+using namespace bh;
+
+extern "C" int bh_knn(const float *x, int64_t n, int64_t d, int64_t k,
+                      int64_t *out_idx, float *out_sqd, bh_stream_t stream) {
+    BH_REQUIRE(k >= 1 && k <= n - 1, "k must be in [1, %lld], got %lld",
+               (long long)(n - 1), (long long)k);
+    BH_REQUIRE(k <= kKnnMaxK, "k must be <= %d for bh_knn", kKnnMaxK);
+    BH_REQUIRE(d >= 1 && d <= 64, "bh_knn supports 1 <= D <= 64, got %lld",
+               (long long)d);
+    const int grid = bh_blocks(n, kKnnThreads);
+    cudaStream_t st = bh_cs(stream);
+    if (d <= 16)
+        k_knn<16><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
+    else if (d <= 32)
+        k_knn<32><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
+    else
+        k_knn<64><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
+    BH_CHECK_LAUNCH("k_knn");
+    return BH_OK;
+}

@@ -1,0 +1,249 @@
+// Stable LSD radix sort of (key, uint32 payload) pairs -- the on-device
+// replacement of _radix_argsort (quadtree.py:188-227).
+//
+// One histogram pass computes every 8-bit digit histogram at once; then one
+// "onesweep" kernel per digit: each CTA claims a tile in launch order, ranks
+// its keys per digit with warp ballots (stable: tile order = index order),
+// publishes its per-digit counts and resolves its global offsets with a
+// decoupled look-back over the previous tiles, stages the tile in shared
+// memory in output order and writes coalesced runs.  Stability makes the
+// permutation equal to np.argsort(keys, kind="stable").
+#include "common.cuh"
+
+namespace bh {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kValMask = (1u << 30) - 1;
+
+template <typename K>
+struct SortCfg {
+    static constexpr int IPT = sizeof(K) == 4 ? 16 : 12;
+    static constexpr int TILE = kSortThreads * IPT;
+    static constexpr size_t SMEM = (size_t)TILE * (sizeof(K) + 4);
+    static_assert(SMEM <= 40 * 1024, "tile must fit the default smem limit");
+};
+
+template <typename K>
+__global__ void __launch_bounds__(256)
+k_sort_hist(const K *__restrict__ keys, int64_t n, int passes,
+            uint32_t *__restrict__ hist) {
+    __shared__ uint32_t sh[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        K k = keys[i];
+        for (int p = 0; p < passes; p++)
+            atomicAdd(&sh[p][(unsigned)(k >> (8 * p)) & 0xFFu], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+        uint32_t c = (&sh[0][0])[i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads)
+k_sort_pass(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
+            K *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
+            int shift, const uint32_t *__restrict__ hist,
+            uint32_t *__restrict__ status, uint32_t *__restrict__ tile_ctr) {
+    constexpr int IPT = SortCfg<K>::IPT, TILE = SortCfg<K>::TILE;
+    extern __shared__ __align__(16) unsigned char smem[];
+    K *s_keys = (K *)smem;
+    uint32_t *s_vals = (uint32_t *)(s_keys + TILE);
+    __shared__ uint32_t s_whist[kSortWarps][256];
+    __shared__ uint32_t s_tile_excl[256], s_glob[256], s_scan[32];
+    __shared__ uint32_t s_tile, s_total;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+#pragma unroll
+    for (int w = 0; w < kSortWarps; w++) s_whist[w][tid] = 0;
+    uint32_t h = hist[tid];
+    uint32_t hx = block_exclusive_scan<uint32_t>(h, s_scan, &s_total);
+    s_glob[tid] = hx;
+    __syncthreads();
+
+    const int64_t base = (int64_t)s_tile * TILE;
+    const int64_t seg = base + (int64_t)warp * 32 * IPT;
+    K k[IPT];
+    uint32_t v[IPT], r[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; j++) {
+        int64_t idx = seg + j * 32 + lane;
+        bool ok = idx < n;
+        k[j] = ok ? kin[idx] : K(0);
+        v[j] = ok ? (vin ? vin[idx] : (uint32_t)idx) : 0u;
+    }
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < IPT; j++) {
+        int64_t idx = seg + j * 32 + lane;
+        bool ok = idx < n;
+        unsigned d = (unsigned)(k[j] >> shift) & 0xFFu;
+        unsigned peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            unsigned bit = (d >> b) & 1u;
+            unsigned bb = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bb : ~bb;
+        }
+        uint32_t old = 0;
+        if (ok) old = s_whist[warp][d];
+        __syncwarp();
+        if (ok && lane == __ffs(peers) - 1) s_whist[warp][d] = old + __popc(peers);
+        __syncwarp();
+        r[j] = old + __popc(peers & lt);
+    }
+    __syncthreads();
+
+    // per digit: exclusive over warps, then over digits (local positions)
+    const int d = tid;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; w++) {
+        uint32_t c = s_whist[w][d];
+        s_whist[w][d] = cnt;
+        cnt += c;
+    }
+    uint32_t te = block_exclusive_scan<uint32_t>(cnt, s_scan, &s_total);
+    s_tile_excl[d] = te;
+
+    // decoupled look-back for this digit's global offset
+    const uint32_t tile = s_tile;
+    uint32_t prefix = 0;
+    if (tile == 0) {
+        st_volatile(&status[d], kFlagP | cnt);
+    } else {
+        st_volatile(&status[(size_t)tile * 256 + d], kFlagA | cnt);
+        int64_t p = (int64_t)tile - 1;
+        while (true) {
+            uint32_t w = ld_volatile(&status[(size_t)p * 256 + d]);
+            uint32_t f = w & ~kValMask;
+            if (f == 0) continue;
+            prefix += w & kValMask;
+            if (f == kFlagP) break;
+            p--;
+        }
+        st_volatile(&status[(size_t)tile * 256 + d], kFlagP | (prefix + cnt));
+    }
+    s_glob[d] += prefix;
+    __syncthreads();
+
+#pragma unroll
+    for (int j = 0; j < IPT; j++) {
+        int64_t idx = seg + j * 32 + lane;
+        if (idx < n) {
+            unsigned dd = (unsigned)(k[j] >> shift) & 0xFFu;
+            uint32_t pos = s_tile_excl[dd] + s_whist[warp][dd] + r[j];
+            s_keys[pos] = k[j];
+            s_vals[pos] = v[j];
+        }
+    }
+    __syncthreads();
+    int64_t rem = n - base;
+    const int valid = rem < TILE ? (int)rem : TILE;
+    for (int i = tid; i < valid; i += kSortThreads) {
+        K kk = s_keys[i];
+        unsigned dd = (unsigned)(kk >> shift) & 0xFFu;
+        int64_t g = (int64_t)s_glob[dd] + (i - (int)s_tile_excl[dd]);
+        kout[g] = kk;
+        vout[g] = s_vals[i];
+    }
+}
+
+struct SortLayout {
+    size_t keys_a, vals_a, keys_b, vals_b, hist, ctr, status, total;
+    int passes;
+    int64_t tiles;
+};
+
+template <typename K>
+static SortLayout sort_layout(int64_t n, int key_bits) {
+    SortLayout L;
+    L.passes = (key_bits + 7) / 8;
+    L.tiles = (n + SortCfg<K>::TILE - 1) / SortCfg<K>::TILE;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += bh_align(bytes);
+        return o;
+    };
+    L.keys_a = take(sizeof(K) * n);
+    L.vals_a = take(4 * n);
+    L.keys_b = take(sizeof(K) * n);
+    L.vals_b = take(4 * n);
+    L.hist = take(4 * 256 * L.passes);
+    L.ctr = take(4 * L.passes);
+    L.status = take(4 * 256 * (size_t)L.tiles * L.passes);
+    L.total = off;
+    return L;
+}
+
+template <typename K>
+static int sort_impl(const K *keys, const uint32_t *vals, int64_t n,
+                     int key_bits, K *out_keys, uint32_t *out_vals, void *ws,
+                     size_t ws_bytes, cudaStream_t st) {
+    BH_REQUIRE(n >= 0 && n < (int64_t)kValMask, "sort size out of range");
+    BH_REQUIRE(key_bits >= 1 && key_bits <= 8 * (int)sizeof(K),
+               "key_bits out of range");
+    if (n == 0) return BH_OK;
+    SortLayout L = sort_layout<K>(n, key_bits);
+    BH_REQUIRE(ws_bytes >= L.total, "sort workspace too small (%zu < %zu)",
+               ws_bytes, L.total);
+    char *w = (char *)ws;
+    uint32_t *hist = (uint32_t *)(w + L.hist);
+    uint32_t *ctr = (uint32_t *)(w + L.ctr);
+    uint32_t *status = (uint32_t *)(w + L.status);
+    cudaError_t e = cudaMemsetAsync(w + L.hist, 0, L.total - L.hist, st);
+    if (e != cudaSuccess) return cuda_status(e, "sort memset");
+    int hb = bh_blocks(n, 256 * 16);
+    if (hb > kSMs * 4) hb = kSMs * 4;
+    k_sort_hist<K><<<hb, 256, 0, st>>>(keys, n, L.passes, hist);
+    BH_CHECK_LAUNCH("k_sort_hist");
+    K *kb[2] = {(K *)(w + L.keys_a), (K *)(w + L.keys_b)};
+    uint32_t *vb[2] = {(uint32_t *)(w + L.vals_a), (uint32_t *)(w + L.vals_b)};
+    for (int p = 0; p < L.passes; p++) {
+        const K *ki = p == 0 ? keys : kb[(p - 1) & 1];
+        const uint32_t *vi = p == 0 ? vals : vb[(p - 1) & 1];
+        K *ko = p == L.passes - 1 ? out_keys : kb[p & 1];
+        uint32_t *vo = p == L.passes - 1 ? out_vals : vb[p & 1];
+        k_sort_pass<K><<<(int)L.tiles, kSortThreads, SortCfg<K>::SMEM, st>>>(
+            ki, vi, ko, vo, n, 8 * p, hist + 256 * p,
+            status + (size_t)256 * L.tiles * p, ctr + p);
+        BH_CHECK_LAUNCH("k_sort_pass");
+    }
+    return BH_OK;
+}
+
+}  // namespace bh
+
+using namespace bh;
+
+extern "C" size_t bh_sort_workspace_bytes(int64_t n, int key_bits) {
+    return key_bits <= 32 ? sort_layout<uint32_t>(n, key_bits).total
+                          : sort_layout<uint64_t>(n, key_bits).total;
+}
+
+extern "C" int bh_sort_pairs(const void *keys, const uint32_t *vals, int64_t n,
+                             int key_bits, void *sorted_keys,
+                             uint32_t *sorted_vals, void *ws, size_t ws_bytes,
+                             bh_stream_t stream) {
+    if (key_bits <= 32)
+        return sort_impl<uint32_t>((const uint32_t *)keys, vals, n, key_bits,
+                                   (uint32_t *)sorted_keys, sorted_vals, ws,
+                                   ws_bytes, bh_cs(stream));
+    return sort_impl<uint64_t>((const uint64_t *)keys, vals, n, key_bits,
+                               (uint64_t *)sorted_keys, sorted_vals, ws,
+                               ws_bytes, bh_cs(stream));
+}
+
+extern "C" int bh_sort(const void *keys, int64_t n, int key_bits,
+                       void *sorted_keys, int32_t *order, void *ws,
+                       size_t ws_bytes, bh_stream_t stream) {
+    return bh_sort_pairs(keys, nullptr, n, key_bits, sorted_keys,
+                         (uint32_t *)order, ws, ws_bytes, stream);
+}

@@ -1,0 +1,28 @@
+"""Exact kNN on the B200 (knn.py:36-73 semantics).
+
+The north star passes the reference's kNN graph in; this kernel exists so
+that ``run(x, cfg)`` without a graph stays a drop-in.  Distances are f64
+column-ordered sums as the reference computes them, ties -> lower id.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream
+from .affinity import NeighborGraph
+
+
+def knn_exact(x, k: int) -> NeighborGraph:
+    data = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)
+                           if not isinstance(x, torch.Tensor) else x)
+    data = data.to(_lib.device(), torch.float32).contiguous()
+    n, d = data.shape
+    if not 1 <= k <= n - 1:
+        raise ValueError(f"k must be in [1, {n - 1}], got {k}")
+    idx = torch.empty((n, k), dtype=torch.int64, device=data.device)
+    sqd = torch.empty((n, k), dtype=torch.float32, device=data.device)
+    call("bh_knn", ptr(data), n, d, k, ptr(idx), ptr(sqd), stream())
+    return NeighborGraph(idx, sqd)

@@ -1,0 +1,454 @@
+"""Gradient-descent driver on the B200: device-resident, CUDA-graph loop.
+
+Mirrors bhtsne.optimizer (reference: pkg/src/bhtsne/optimizer.py):
+``TsneConfig`` (:43-83), ``Embedding`` (:86-113), ``StepTimings``
+(:116-144), ``init_embedding`` (:147-158), ``gradient_step`` (:195-224),
+``kl_divergence`` (:242-270) and ``run`` (:289-332), same defaults, argument
+meaning and error messages.  Differences, all deliberate:
+
+* arrays are CUDA tensors ((N, 2) float32 for y / velocity / gains);
+* ``precision`` is "f32" only (the north-star path computes in float32 with
+  float64 accumulation);
+* ``run`` takes the kNN graph (``knn=``) computed once by the reference, as
+  the north star specifies, or computes it with the exact GPU kNN;
+* ``code_bits`` selects 32-bit Morton codes (default) or the reference's
+  64-bit codes.
+
+The hot loop (:318-325) runs as CUDA-graph replays of ``graph_chunk``
+iterations: bounds -> Morton -> radix sort -> tree -> summarize ->
+attractive -> repulsive -> update, with the exaggeration / momentum schedule
+read from a device-side ``bh_sched_t`` and stage times taken from external
+CUDA events captured in the graph (exact per-iteration StepTimings).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BOUNDS_DTYPE, SCHED_DTYPE, INT64_MAX, call, ptr, stream
+from .affinity import (SparseAffinity, as_graph, calibrate_perplexity,
+                       set_exaggeration, symmetrize)
+from .forces import GradientBuffers, repulsive_bh, repulsive_exact
+from .quadtree import (DEFAULT_CODE_BITS, TreeArrays, as_points, build_tree,
+                       compute_bounds, morton_codes, summarize)
+
+STAGES = ("knn", "bsp", "tree", "summarize", "attractive", "repulsive",
+          "update")
+EXTRA_STAGES = ("comm",)
+MOMENTUM_SWITCH_ITER = 250
+PRECISIONS = ("f32",)
+
+
+@dataclass
+class TsneConfig:
+    perplexity: float = 30.0
+    theta: float = 0.5
+    n_iter: int = 1000
+    early_exaggeration: float = 12.0
+    exaggeration_iters: int = 250
+    learning_rate: float = 200.0
+    momentum_early: float = 0.5
+    momentum_late: float = 0.8
+    min_gain: float = 0.01
+    seed: int = 0
+    precision: str = "f32"
+    threads: int | None = None  # accepted for compatibility; unused on GPU
+    kl_every: int = 0
+    code_bits: int = DEFAULT_CODE_BITS
+    graph_chunk: int = 25
+
+    def validate(self) -> "TsneConfig":
+        if self.perplexity <= 1:
+            raise ValueError(
+                f"perplexity must be > 1, got {self.perplexity}")
+        if self.theta < 0:
+            raise ValueError(f"theta must be >= 0, got {self.theta}")
+        if self.learning_rate <= 0:
+            raise ValueError(
+                f"learning rate must be > 0, got {self.learning_rate}")
+        if self.n_iter < 0:
+            raise ValueError(f"n_iter must be >= 0, got {self.n_iter}")
+        if self.n_iter < self.exaggeration_iters:
+            raise ValueError(
+                f"n_iter ({self.n_iter}) must cover the exaggeration phase "
+                f"({self.exaggeration_iters} iterations)")
+        if self.early_exaggeration <= 0:
+            raise ValueError("early exaggeration must be > 0")
+        if self.precision not in PRECISIONS:
+            raise ValueError(
+                f"unknown precision {self.precision!r}; expected one of "
+                f"{list(PRECISIONS)} (the B200 path is float32)")
+        if self.threads is not None and self.threads < 1:
+            raise ValueError(f"threads must be >= 1, got {self.threads}")
+        if self.code_bits not in (32, 64):
+            raise ValueError(f"code_bits must be 32 or 64, got {self.code_bits}")
+        if self.graph_chunk < 1:
+            raise ValueError("graph_chunk must be >= 1")
+        return self
+
+    @property
+    def dtype(self):
+        return np.dtype(np.float32)
+
+
+@dataclass
+class Embedding:
+    """(N, 2) points plus optimizer state, resident on the device."""
+
+    y: torch.Tensor   # (N, 2) float32
+    v: torch.Tensor   # velocity
+    g: torch.Tensor   # adaptive gains (start at 1)
+    iteration: int = 0
+    rng_seed: int = 0
+
+    @property
+    def n_points(self) -> int:
+        return self.y.shape[0]
+
+    y0 = property(lambda s: s.y[:, 0])
+    y1 = property(lambda s: s.y[:, 1])
+    v0 = property(lambda s: s.v[:, 0])
+    v1 = property(lambda s: s.v[:, 1])
+    g0 = property(lambda s: s.g[:, 0])
+    g1 = property(lambda s: s.g[:, 1])
+
+    @property
+    def velocity(self) -> torch.Tensor:
+        return self.v
+
+    @property
+    def gains(self) -> torch.Tensor:
+        return self.g
+
+    def numpy(self) -> np.ndarray:
+        return self.y.cpu().numpy()
+
+
+@dataclass
+class StepTimings:
+    """Wall time per pipeline stage, per call and cumulative (seconds)."""
+
+    per_call: dict = field(
+        default_factory=lambda: {s: [] for s in STAGES + EXTRA_STAGES})
+    total_wall_s: float = 0.0
+    kl_history: list = field(default_factory=list)
+
+    def add(self, stage: str, seconds: float) -> None:
+        self.per_call[stage].append(seconds)
+
+    def total(self, stage: str) -> float:
+        return math.fsum(self.per_call[stage])
+
+    def calls(self, stage: str) -> int:
+        return len(self.per_call[stage])
+
+    def report(self) -> dict:
+        out = {}
+        for stage in STAGES + EXTRA_STAGES:
+            calls = self.calls(stage)
+            total = self.total(stage)
+            out[stage] = {"total_s": total,
+                          "per_iter_mean_s": total / calls if calls else 0.0,
+                          "calls": calls}
+        return out
+
+
+def init_embedding(n: int, seed: int, dtype=np.float32) -> Embedding:
+    """Gaussian init (sd 1e-4) from numpy's Philox(seed), as the reference,
+    generated on the host (bit-identical Y0) and uploaded once."""
+    if n < 2:
+        raise ValueError(f"need at least 2 points, got {n}")
+    if np.dtype(dtype) != np.float32:
+        raise ValueError("the B200 path is float32")
+    rng = np.random.Generator(np.random.Philox(seed))
+    y = (rng.standard_normal((n, 2)) * 1e-4).astype(np.float32)
+    dev = _lib.device()
+    yt = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
+    return Embedding(y=yt, v=torch.zeros_like(yt), g=torch.ones_like(yt),
+                     iteration=0, rng_seed=int(seed))
+
+
+def embedding_from(y, v=None, g=None, iteration=0) -> Embedding:
+    pts = as_points(y).clone()
+    return Embedding(y=pts,
+                     v=torch.zeros_like(pts) if v is None else as_points(v).clone(),
+                     g=torch.ones_like(pts) if g is None else as_points(g).clone(),
+                     iteration=iteration)
+
+
+# ---------------------------------------------------------------------------
+# Engine: all buffers of the loop preallocated; one iteration = 8 launches
+# (+ 3 sort passes) enqueued on the current stream; graph-captured.
+# ---------------------------------------------------------------------------
+class Engine:
+    def __init__(self, p: SparseAffinity, e: Embedding, cfg: TsneConfig,
+                 schedule: bool = True, shard=None):
+        lib = _lib.load()
+        n = e.n_points
+        if p.n != n:
+            raise ValueError(f"matrix is over {p.n} points, embedding has {n}")
+        self.n, self.cfg, self.e, self.p = n, cfg, e, p
+        self.code_bits = cfg.code_bits
+        dev = e.y.device
+        self.dev = dev
+        self.rp, self.col, self.val = p.padded()
+        self.attr = torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        self.rep = torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        exag_on = schedule and cfg.n_iter > 0 and cfg.exaggeration_iters > 0
+        self.sched = _lib.struct_tensor(SCHED_DTYPE, dict(
+            iteration=e.iteration,
+            exaggeration_iters=cfg.exaggeration_iters if exag_on else 0,
+            momentum_switch=MOMENTUM_SWITCH_ITER,
+            exaggeration=np.float32(cfg.early_exaggeration),
+            momentum_early=cfg.momentum_early,
+            momentum_late=cfg.momentum_late,
+            learning_rate=cfg.learning_rate, min_gain=cfg.min_gain,
+            bad=INT64_MAX, z=0.0))
+        self.bounds = _lib.struct_tensor(BOUNDS_DTYPE)
+        self.codes = torch.zeros(
+            n, dtype=torch.int32 if self.code_bits == 32 else torch.int64,
+            device=dev)
+        self.tree = TreeArrays(n, self.code_bits, dev)
+        self.ws_sort = _lib.workspace(lib.bh_sort_workspace_bytes(n, self.code_bits))
+        self.ws_rep = _lib.workspace(lib.bh_repulsive_workspace_bytes(n))
+        self.ws_upd = _lib.workspace(lib.bh_update_workspace_bytes(n))
+        self.ws_bnd = _lib.workspace(lib.bh_bounds_workspace_bytes(n))
+        self.z_dev = self.sched[48:56].view(torch.float64)  # sched.z
+        self.theta = float(cfg.theta)
+        self.graphs = {}
+        self.shard = shard
+        if shard is not None:
+            shard.attach(self)
+
+    # -- one iteration -----------------------------------------------------
+    # events: 0 start | 1 tree built | 2 summarized | 3 attractive |
+    #         4 repulsive | 5 exchange done (multi-GPU) | 6 updated
+    N_EVENTS = 7
+    STAGE_EVENTS = {"tree": (0, 1), "summarize": (1, 2), "attractive": (2, 3),
+                    "repulsive": (3, 4), "update": (5, 6)}
+
+    def kernels_per_iteration(self) -> int:
+        """Kernel launches of one iteration (morton, sort histogram + one
+        pass per byte, 3 tree kernels, summarize, attractive, repulsive,
+        update; + the Z-partials sum when sharded)."""
+        return 1 + 1 + self.code_bits // 8 + 3 + 1 + 1 + 1 + 1 + (
+            1 if self.shard is not None else 0)
+
+    def _enqueue(self, ev=None):
+        st = stream()
+        n, cb, t = self.n, self.code_bits, self.tree
+        y = self.e.y
+        rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
+        rec(0)
+        call("bh_morton", ptr(y), n, ptr(self.bounds), cb, 1, ptr(self.codes), st)
+        call("bh_sort", ptr(self.codes), n, cb, ptr(t.sorted_codes),
+             ptr(t.order), ptr(self.ws_sort), self.ws_sort.numel(), st)
+        t.build(y, st)
+        rec(1)
+        t.summarize(st)
+        rec(2)
+        if self.shard is None:
+            call("bh_attractive", ptr(self.rp), ptr(self.col), ptr(self.val), n,
+                 1, ptr(y), 0, n, 1.0, ptr(self.sched), ptr(self.attr), st)
+            rec(3)
+            call("bh_repulsive", t.sref(), ptr(self.bounds), self.theta, None,
+                 0, n, 0, ptr(self.rep), None, None, ptr(self.z_dev), None,
+                 ptr(self.ws_rep), self.ws_rep.numel(), st)
+            rec(4)
+            rec(5)
+            rep, rep_rank = self.rep, None
+        else:
+            rep, rep_rank = self.shard.forces(self, rec, st)
+        call("bh_update", ptr(y), ptr(self.e.v), ptr(self.e.g), ptr(self.attr),
+             ptr(rep), ptr(rep_rank), n, ptr(self.sched), ptr(self.bounds), cb,
+             ptr(self.ws_upd), self.ws_upd.numel(), st)
+        rec(6)
+
+    def _events(self, k):
+        return [[torch.cuda.Event(enable_timing=True, external=True)
+                 for _ in range(self.N_EVENTS)] for _ in range(k)]
+
+    def _graph(self, k):
+        if k not in self.graphs:
+            evs = self._events(k)
+            g = torch.cuda.CUDAGraph()
+            # the loop keeps no allocator state: capture straight away
+            with torch.cuda.graph(g):
+                for i in range(k):
+                    self._enqueue(evs[i])
+            self.graphs[k] = (g, evs)
+        return self.graphs[k]
+
+    def begin(self):
+        """Bounds of the current (centred) Y, shift 0."""
+        call("bh_bounds", ptr(self.e.y), self.n, self.code_bits,
+             ptr(self.bounds), ptr(self.ws_bnd), self.ws_bnd.numel(), stream())
+
+    def end(self):
+        """Apply the pending re-centering of the last update."""
+        call("bh_center", ptr(self.e.y), self.n, ptr(self.bounds), stream())
+
+    def set_iteration(self, it: int, exaggeration: float | None = None):
+        """Host override of the schedule (stage API: p carries the factor)."""
+        host = _lib.read_struct(self.sched, SCHED_DTYPE).copy()
+        host["iteration"] = it
+        if exaggeration is not None:
+            host["exaggeration"] = np.float32(exaggeration)
+            host["exaggeration_iters"] = np.iinfo(np.int32).max
+        self.sched.copy_(torch.from_numpy(
+            np.array([host], SCHED_DTYPE).view(np.uint8)).to(self.dev))
+
+    def _check(self):
+        s = _lib.read_struct(self.sched, SCHED_DTYPE)
+        if int(s["bad"]) != INT64_MAX:
+            bad = int(s["bad"])
+            raise ValueError(f"non-finite gradient at point {bad & 0xFFFFFFFF} "
+                             f"(iteration {bad >> 32})")
+        if int(self.tree.status.item()) != 0:
+            raise RuntimeError("quadtree node capacity exceeded")
+        return s
+
+    def run(self, n_iter: int, timings: StepTimings | None = None,
+            use_graph: bool = True):
+        """Advance n_iter iterations; Y is centred on return."""
+        if n_iter <= 0:
+            return
+        self.begin()
+        done = 0
+        chunk = self.cfg.graph_chunk
+        while done < n_iter:
+            k = min(chunk, n_iter - done)
+            if use_graph:
+                g, evs = self._graph(k)
+                g.replay()
+            else:
+                evs = self._events(k)
+                for i in range(k):
+                    self._enqueue(evs[i])
+            evs[-1][-1].synchronize()
+            self._check()
+            if timings is not None:
+                for i in range(k):
+                    for name, (a, b) in self.STAGE_EVENTS.items():
+                        timings.add(name, evs[i][a].elapsed_time(evs[i][b]) * 1e-3)
+                    if self.shard is not None:
+                        timings.add("comm", evs[i][4].elapsed_time(evs[i][5]) * 1e-3)
+            done += k
+        self.end()
+        self.e.iteration += n_iter
+
+    @property
+    def z(self) -> float:
+        return float(_lib.read_struct(self.sched, SCHED_DTYPE)["z"])
+
+
+def gradient_step(e: Embedding, p: SparseAffinity, cfg: TsneConfig,
+                  buffers: GradientBuffers | None = None,
+                  timings: StepTimings | None = None) -> Embedding:
+    """One full iteration: tree, summarize, forces, momentum update
+    (optimizer.py:195-224); the exaggeration is the one ``p`` carries."""
+    cfg.validate()
+    eng = getattr(e, "_engine", None)
+    if (eng is None or eng.p.base_values is not p.base_values
+            or eng.cfg is not cfg):
+        eng = Engine(p, e, cfg, schedule=False)
+        e._engine = eng
+    eng.set_iteration(e.iteration, exaggeration=p.exaggeration)
+    eng.run(1, timings, use_graph=False)
+    if buffers is not None:
+        buffers.attr.copy_(eng.attr)
+        buffers.rep.copy_(eng.rep)
+        buffers.z_dev.copy_(eng.z_dev)
+    return e
+
+
+def kl_divergence(p: SparseAffinity, y, mode: str = "exact",
+                  theta: float = 0.5) -> float:
+    """C = sum p_ij ln(p_ij / q_ij) over the nonzeros of p
+    (optimizer.py:242-270); Z exact (O(N^2) kernel) or Barnes-Hut."""
+    if p.exaggeration != 1.0:
+        raise ValueError(
+            f"KL divergence requires exaggeration 1, got {p.exaggeration}")
+    pts = as_points(y)
+    n = pts.shape[0]
+    if p.n != n:
+        raise ValueError(f"matrix is over {p.n} points, embedding has {n}")
+    buffers = GradientBuffers.allocate(n)
+    if mode == "exact":
+        repulsive_exact(pts, buffers)
+    elif mode == "bh":
+        center, r_span = compute_bounds(pts)
+        tree = build_tree(morton_codes(pts, center, r_span), pts)
+        summarize(tree)
+        repulsive_bh(tree, pts, theta, buffers)
+    else:
+        raise ValueError(f"unknown mode {mode!r}; expected 'exact' or 'bh'")
+    lib = _lib.load()
+    out = torch.zeros(1, dtype=torch.float64, device=pts.device)
+    ws = _lib.workspace(lib.bh_kl_workspace_bytes(n))
+    call("bh_kl_rows", ptr(p.row_offsets), ptr(p.col_indices),
+         ptr(p.base_values), n, 0, ptr(pts), ptr(buffers.z_dev), ptr(out),
+         ptr(ws), ws.numel(), stream())
+    return float(out.item())
+
+
+def affinities(x, cfg: TsneConfig, knn=None, timings=None):
+    """kNN graph (given, or exact on the GPU) -> BSP -> symmetrised P."""
+    tick = time.perf_counter
+    if knn is None:
+        from .knn import knn_exact
+        data = np.ascontiguousarray(getattr(x, "data", x), dtype=np.float32)
+        n = data.shape[0]
+        k = min(int(math.floor(3 * cfg.perplexity)), n - 1)
+        t0 = tick()
+        knn = knn_exact(data, k)
+        torch.cuda.synchronize()
+        if timings is not None:
+            timings.add("knn", tick() - t0)
+    elif timings is not None:
+        timings.add("knn", 0.0)
+    graph = as_graph(knn)
+    t0 = tick()
+    pr = calibrate_perplexity(graph, cfg.perplexity)
+    p = symmetrize(pr, graph)
+    torch.cuda.synchronize()
+    if timings is not None:
+        timings.add("bsp", tick() - t0)
+    return p, graph
+
+
+def run(x, cfg: TsneConfig, *, knn=None) -> tuple:
+    """Full pipeline; returns (embedding, timings, final exact KL)
+    (optimizer.py:289-332).  ``knn``: a NeighborGraph / (indices,
+    sq_distances) computed once by the reference (north star), else the
+    exact kNN is computed on the GPU."""
+    cfg.validate()
+    tick = time.perf_counter
+    wall0 = tick()
+    timings = StepTimings()
+    data = getattr(x, "data", x)
+    n = int(np.shape(data)[0]) if knn is None else as_graph(knn).n_points
+    p, _ = affinities(x, cfg, knn=knn, timings=timings)
+    e = init_embedding(n, cfg.seed)
+    eng = Engine(p, e, cfg, schedule=True)
+    kl_history = []
+    done = 0
+    while done < cfg.n_iter:
+        step = cfg.n_iter - done
+        if cfg.kl_every:
+            step = min(step, cfg.kl_every - done % cfg.kl_every)
+        eng.run(step, timings)
+        done += step
+        if cfg.kl_every and done % cfg.kl_every == 0:
+            kl_history.append((done, kl_divergence(p, e.y, mode="bh",
+                                                   theta=cfg.theta)))
+    kl = kl_divergence(p, e.y, mode="exact")
+    timings.total_wall_s = tick() - wall0
+    timings.kl_history.extend(kl_history)
+    return e, timings, kl

@@ -1,0 +1,362 @@
+"""GPU parity: every stage of the CUDA path against the CPU oracle and the
+reference's golden vectors, through the C ABI.
+
+Tolerances (north star): Morton codes, permutation, tree topology, masses
+and centres of mass bit-exact; per-iteration gradients <= 1e-4 relative L2;
+BSP betas <= 1e-5 relative; final KL within 1%.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import TREE_CASES, golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOPO = ("level_offsets", "start", "end", "children", "is_leaf", "cell_center",
+        "cell_radius", "mass", "com", "order", "ys0", "ys1")
+
+
+@pytest.fixture(scope="module")
+def bh():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2212_11506_b200 as m
+    return m
+
+
+def gpu_tree(bh, y, code_bits):
+    c, r = bh.compute_bounds(y, code_bits)
+    mc = bh.morton_codes(y, c, r, code_bits)
+    t = bh.summarize(bh.build_tree(mc, y))
+    return (c, r), mc, t
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# --- Morton / sort / tree: bit-exact against the reference goldens -------
+
+@pytest.mark.parametrize("mode", [32, 64])
+@pytest.mark.parametrize("case", TREE_CASES)
+def test_tree_bit_exact_vs_reference_golden(bh, mode, case):
+    g = golden(f"tree{mode}_{case}")
+    y = g["y"]
+    (c, r), mc, t = gpu_tree(bh, y, mode)
+    assert c == tuple(g["center"]) and r == float(g["r_span"])
+    ref_codes = g["codes"] if mode == 64 else g["codes"] >> np.uint64(32)
+    np.testing.assert_array_equal(mc.codes_u64(), ref_codes)
+    np.testing.assert_array_equal(mc.order.cpu().numpy(), g["order"])
+    out = t.to_reference()
+    for f in TOPO:
+        np.testing.assert_array_equal(out[f], g[f], err_msg=f)
+
+
+def test_golden_dump(bh):
+    g = golden("tree64_dump4")
+    _, _, t = gpu_tree(bh, g["y"], 64)
+    assert t.dump() == str(g["dump"])
+
+
+@pytest.mark.parametrize("mode", [32, 64])
+@pytest.mark.parametrize("kind", ["gauss", "heavy", "dups", "tiny_spread"])
+def test_tree_bit_exact_vs_oracle_large(bh, oracle, mode, kind):
+    rng = np.random.default_rng(hash((mode, kind)) % 2**32)
+    n = 120_000
+    if kind == "gauss":
+        y = rng.standard_normal((n, 2))
+    elif kind == "heavy":
+        c = rng.uniform(-50, 50, (100, 2))
+        y = c[rng.integers(0, 100, n)] + rng.standard_t(2.0, (n, 2))
+    elif kind == "dups":
+        base = rng.standard_normal((n // 50, 2))
+        y = base[rng.integers(0, n // 50, n)]
+    else:
+        y = 1e3 + rng.standard_normal((n, 2)) * 1e-5
+    y = y.astype(np.float32)
+    (c, r), mc, t = gpu_tree(bh, y, mode)
+    assert (c, r) == oracle.compute_bounds(y)
+    codes, order, sc = oracle.morton_codes(y, c, r, mode)
+    np.testing.assert_array_equal(mc.codes_u64(), codes)
+    np.testing.assert_array_equal(mc.order.cpu().numpy(), order)
+    ot = oracle.tree_from_sorted(sc, order, y, c, r, mode)
+    out = t.to_reference()
+    for f in TOPO:
+        np.testing.assert_array_equal(out[f], getattr(ot, f), err_msg=f)
+
+
+@pytest.mark.parametrize("bits", [8, 17, 32, 42, 64])
+def test_radix_sort_is_stable_argsort(bh, bits):
+    from paper_2212_11506_b200 import _lib
+    rng = np.random.default_rng(bits)
+    n = 300_001
+    hi = (1 << bits) - 1
+    keys = rng.integers(0, min(hi, 2**63 - 1), n, dtype=np.int64).astype(np.uint64)
+    keys[::7] = keys[0]  # heavy duplicates
+    dt = np.uint32 if bits <= 32 else np.uint64
+    keys = keys.astype(dt)
+    kd = torch.from_numpy(keys.view(np.int32 if bits <= 32 else np.int64)).cuda()
+    sk = torch.empty_like(kd)
+    order = torch.empty(n, dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    ws = _lib.workspace(lib.bh_sort_workspace_bytes(n, bits))
+    for _ in range(2):  # workspace reuse must leave counters at zero
+        _lib.call("bh_sort", _lib.ptr(kd), n, bits, _lib.ptr(sk),
+                  _lib.ptr(order), _lib.ptr(ws), ws.numel(), _lib.stream())
+        ref = np.argsort(keys, kind="stable")
+        np.testing.assert_array_equal(order.cpu().numpy(), ref)
+        np.testing.assert_array_equal(sk.cpu().numpy().view(dt), keys[ref])
+
+
+# --- forces ---------------------------------------------------------------
+
+@pytest.mark.parametrize("mode", [32, 64])
+@pytest.mark.parametrize("case", ["gauss2000", "heavy3200", "coinc7", "two",
+                                  "quad4"])
+@pytest.mark.parametrize("theta", [0.0, 0.5, 0.8])
+def test_repulsive_vs_reference_golden(bh, mode, case, theta):
+    g = golden(f"tree{mode}_{case}")
+    y = g["y"]
+    _, _, t = gpu_tree(bh, y, mode)
+    buf = bh.GradientBuffers.allocate(y.shape[0])
+    bh.repulsive_bh(t, y, theta, buf)
+    tag = f"bh{int(theta * 10)}"
+    ref = np.column_stack([g[tag + "_rep0"], g[tag + "_rep1"]])
+    got = buf.rep.cpu().numpy()
+    # f32 pair math vs the reference's f64: per-point relative error
+    norm = np.linalg.norm(ref, axis=1)
+    err = np.linalg.norm(got - ref, axis=1)
+    assert (err <= 2e-5 * np.maximum(norm, 1e-3 * norm.max()) + 1e-30).all()
+    np.testing.assert_allclose(buf.z_partial.cpu().numpy(), g[tag + "_zpart"],
+                               rtol=2e-6)
+    assert buf.z == pytest.approx(float(g[tag + "_z"]), rel=1e-6)
+
+
+@pytest.mark.parametrize("mode", [32, 64])
+def test_repulsive_large_vs_oracle(bh, oracle, mode):
+    rng = np.random.default_rng(3)
+    c = rng.uniform(-50, 50, (100, 2))
+    y = (c[rng.integers(0, 100, 200_000)]
+         + rng.standard_t(2.0, (200_000, 2))).astype(np.float32)
+    _, _, t = gpu_tree(bh, y, mode)
+    buf = bh.GradientBuffers.allocate(y.shape[0])
+    bh.repulsive_bh(t, y, 0.5, buf)
+    ot = oracle.build_tree(y, code_bits=mode)
+    r0, r1, zp, z = oracle.repulsive_bh(ot, y, 0.5)
+    ref = np.column_stack([r0, r1])
+    assert rel_l2(buf.rep.cpu().numpy(), ref) < 1e-5
+    assert buf.z == pytest.approx(z, rel=1e-7)
+    cnt = bh.repulsive_counts(t, 0.5)
+    _, _, _, _, oc = oracle.repulsive_bh(ot, y, 0.5, counts=True)
+    # per-point visit counts equal the reference traversal's (exact BH
+    # semantics of the warp-synchronous walk); f32 vs f64 accept decisions
+    # may flip on a handful of boundary cases
+    mism = (cnt[:, 0] != oc[:, 0]).mean()
+    assert mism < 1e-3
+    assert abs(cnt[:, 0].sum() - oc[:, 0].sum()) / oc[:, 0].sum() < 1e-4
+
+
+def test_repulsive_theta0_equals_exact(bh):
+    rng = np.random.default_rng(11)
+    y = rng.standard_normal((500, 2)).astype(np.float32)
+    _, _, t = gpu_tree(bh, y, 32)
+    bhb = bh.GradientBuffers.allocate(500)
+    bh.repulsive_bh(t, y, 0.0, bhb)
+    ex = bh.GradientBuffers.allocate(500)
+    bh.repulsive_exact(y, ex)
+    assert rel_l2(bhb.rep.cpu().numpy(), ex.rep.cpu().numpy()) < 1e-6
+    assert bhb.z == pytest.approx(ex.z, rel=1e-7)
+
+
+def test_attractive_vs_reference_golden(bh):
+    g = golden("affinity450")
+    p = bh.from_csr(g["row_offsets"], g["col_indices"], g["values"])
+    for fac, a0, a1 in ((1.0, "attr0", "attr1"), (12.0, "attr12_0", "attr12_1")):
+        buf = bh.GradientBuffers.allocate(450)
+        bh.attractive(bh.set_exaggeration(p, fac), g["y"], buf)
+        ref = np.column_stack([g[a0], g[a1]])
+        assert rel_l2(buf.attr.cpu().numpy(), ref) < 1e-6
+
+
+def test_attractive_two_point_and_empty_row(bh):
+    p = bh.from_csr([0, 1, 2, 2], [1, 0], np.array([0.5, 0.5], np.float32))
+    y = np.array([[0.0, 0.0], [1.0, 0.0], [5.0, 5.0]], np.float32)
+    buf = bh.GradientBuffers.allocate(3)
+    bh.attractive(p, y, buf)
+    np.testing.assert_allclose(buf.attr.cpu().numpy(),
+                               [[-0.25, 0.0], [0.25, 0.0], [0.0, 0.0]],
+                               atol=1e-7)
+    with pytest.raises(ValueError, match="matrix is over 3 points"):
+        bh.attractive(p, y[:2], buf)
+
+
+# --- affinities -----------------------------------------------------------
+
+def test_bsp_and_symmetrize_vs_reference_golden(bh):
+    g = golden("affinity450")
+    graph = bh.NeighborGraph(g["indices"], g["sq_distances"])
+    pr = bh.calibrate_perplexity(graph, 10.0)
+    betas = pr.betas.cpu().numpy()
+    assert np.max(np.abs(betas - g["betas"]) / g["betas"]) <= 1e-5
+    np.testing.assert_allclose(pr.conditional.cpu().numpy(), g["cond"],
+                               rtol=1e-9, atol=1e-300)
+    p = bh.symmetrize(pr, graph)
+    ro, co, va = p.to_reference()
+    np.testing.assert_array_equal(ro, g["row_offsets"])
+    np.testing.assert_array_equal(co, g["col_indices"])
+    # values: same f64 sums, cast to f32 -> equal up to one f32 ulp
+    np.testing.assert_allclose(va, g["values"], rtol=1.2e-7, atol=0)
+    # symmetric with bitwise-equal values (test_affinity.py:148-164)
+    rows = np.repeat(np.arange(450), np.diff(ro))
+    d = {(r, c): v for r, c, v in zip(rows, co, va)}
+    assert all(d[(c, r)] == v for (r, c), v in d.items())
+
+
+def test_symmetrize_exact_from_reference_conditionals(bh):
+    """Fed the reference's own conditionals, the CSR is bit-identical."""
+    g = golden("affinity450")
+    graph = bh.NeighborGraph(g["indices"], g["sq_distances"])
+    from paper_2212_11506_b200.affinity import PerplexityResult
+    pr = PerplexityResult(betas=torch.from_numpy(g["betas"]).cuda(),
+                          conditional=torch.from_numpy(g["cond"]).cuda())
+    ro, co, va = bh.symmetrize(pr, graph).to_reference()
+    np.testing.assert_array_equal(va, g["values"])
+
+
+def test_bsp_edge_cases(bh):
+    g = bh.NeighborGraph(np.array([[1, 2]]), np.array([[4.0, 4.0]]))
+    pr = bh.calibrate_perplexity(g, 2.0)
+    np.testing.assert_array_equal(pr.conditional.cpu().numpy()[0], [0.5, 0.5])
+    g = bh.NeighborGraph(np.array([[1, 2, 3]]), np.zeros((1, 3)))
+    pr = bh.calibrate_perplexity(g, 2.0)
+    np.testing.assert_allclose(pr.conditional.cpu().numpy()[0], 1 / 3)
+    with pytest.raises(ValueError, match="perplexity exceeds neighborhood"):
+        bh.calibrate_perplexity(bh.NeighborGraph(np.array([[1, 2]]),
+                                                 np.array([[1.0, 2.0]])), 3.0)
+
+
+def test_knn_exact_vs_reference(bh):
+    from paper_2212_11506_b200.knn import knn_exact
+    g = golden("affinity450")
+    kg = knn_exact(g["x"], 30)
+    np.testing.assert_array_equal(kg.indices.cpu().numpy(), g["indices"])
+    np.testing.assert_array_equal(kg.sq_distances.cpu().numpy(),
+                                  g["sq_distances"])
+    from paper_2212_11506_b200.workloads import c0
+    kg = knn_exact(c0(), 90)
+    np.testing.assert_array_equal(kg.indices.cpu().numpy(),
+                                  golden("c0_run")["indices"].astype(np.int64))
+
+
+# --- optimiser ------------------------------------------------------------
+
+def test_gradient_step_trajectory_vs_reference(bh):
+    """Eight reference gradient_step calls (exaggerated, then across the
+    momentum switch) on the same P: gradients match to <= 1e-4 rel-L2 at
+    every step, so the trajectories stay together."""
+    a = golden("affinity450")
+    g = golden("trajectory450")
+    p = bh.from_csr(a["row_offsets"], a["col_indices"], a["values"])
+    pe = bh.set_exaggeration(p, 12.0)
+    e = bh.embedding_from(np.column_stack([g["y0_init"], g["y1_init"]]))
+    cfg = bh.TsneConfig(perplexity=10.0, code_bits=64)
+    for it in range(8):
+        if it == 4:
+            e.iteration = 250
+        bh.gradient_step(e, pe if it < 4 else p, cfg)
+        ref = np.column_stack([g[f"y0_{it}"], g[f"y1_{it}"]])
+        assert rel_l2(e.y.cpu().numpy(), ref) < 1e-5, it
+
+
+@pytest.mark.parametrize("code_bits", [32, 64])
+def test_gradient_parity_late_iterations(bh, oracle, code_bits):
+    """Run the oracle to iterations {0, 250, 500, 999} of the C0 schedule and
+    compare the GPU gradient on the same Y snapshot (rel-L2 <= 1e-4)."""
+    from paper_2212_11506_b200.workloads import c0
+    x = c0()
+    idx, sqd = oracle.knn_exact(x, 90)
+    betas, cond = oracle.calibrate_perplexity(sqd, 30.0)
+    ro, co, va = oracle.symmetrize(idx, cond)
+    p = bh.from_csr(ro, co, va)
+    s = oracle.State.init(2048, 0)
+    checkpoints = {0, 250, 500, 999}
+    for it in range(1000):
+        vals = oracle.exaggerate(va, 12.0) if it < 250 else va
+        if it in checkpoints:
+            y = np.column_stack([s.y0, s.y1])
+            g0, g1, _, _, _ = oracle.gradient(y, ro, co, vals, 0.5, code_bits)
+            ref = np.column_stack([g0, g1])
+            pp = bh.set_exaggeration(p, 12.0 if it < 250 else 1.0)
+            (c, r), mc, t = gpu_tree(bh, y, code_bits)
+            buf = bh.GradientBuffers.allocate(2048)
+            bh.attractive(pp, y, buf)
+            bh.repulsive_bh(t, y, 0.5, buf)
+            zf = np.float32(buf.z)
+            got = np.float32(4.0) * (buf.attr.cpu().numpy()
+                                     - buf.rep.cpu().numpy() / zf)
+            assert rel_l2(got, ref) <= 1e-4, (it, rel_l2(got, ref))
+        oracle.gradient_step(s, ro, co, vals, code_bits=code_bits)
+
+
+def test_engine_graph_equals_eager_and_is_deterministic(bh):
+    a = golden("affinity450")
+    p = bh.from_csr(a["row_offsets"], a["col_indices"], a["values"])
+    outs = []
+    for use_graph in (True, True, False):
+        e = bh.init_embedding(450, seed=3)
+        cfg = bh.TsneConfig(n_iter=60, exaggeration_iters=20, graph_chunk=7)
+        eng = bh.Engine(p, e, cfg)
+        eng.run(60, use_graph=use_graph)
+        outs.append(e.y.cpu().numpy().copy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
+
+
+def test_non_finite_gradient_reports_point(bh):
+    p = bh.from_csr([0, 1, 2], [1, 0], np.array([0.5, 0.5], np.float32))
+    e = bh.embedding_from(np.array([[-1e30, 0.0], [1e30, 0.0]], np.float32))
+    with pytest.raises(ValueError, match="non-finite gradient at point 0"):
+        bh.gradient_step(e, p, bh.TsneConfig(n_iter=10, exaggeration_iters=0))
+
+
+def test_recentred_and_momentum_switch(bh):
+    p = bh.from_csr([0, 1, 2], [1, 0], np.array([0.5, 0.5], np.float32))
+    for it, mom in ((249, 0.5), (250, 0.8)):
+        e = bh.embedding_from(np.array([[-0.5, 0.0], [0.5, 0.0]], np.float32),
+                              v=np.array([[0.02, 0.0], [-0.01, 0.0]], np.float32))
+        e.iteration = it
+        v_before = e.v.cpu().numpy().copy()
+        bh.gradient_step(e, p, bh.TsneConfig(n_iter=300, theta=0.0))
+        np.testing.assert_allclose(e.v.cpu().numpy()[:, 0],
+                                   mom * v_before[:, 0], atol=1e-7)
+        assert abs(float(e.y[:, 0].double().mean())) < 1e-7
+
+
+@pytest.mark.slow
+def test_c0_full_run_kl_within_1pct(bh):
+    from paper_2212_11506_b200.workloads import c0
+    g = golden("c0_run")
+    knn = (g["indices"].astype(np.int64), None)
+    from oracle import oracle as o
+    idx, sqd = o.knn_exact(c0(), 90)
+    e, timings, kl = bh.run(c0(), bh.TsneConfig(kl_every=250),
+                            knn=(idx, sqd))
+    assert abs(kl - float(g["kl"])) / float(g["kl"]) < 0.01, kl
+    assert timings.calls("tree") == 1000
+    assert [it for it, _ in timings.kl_history] == [250, 500, 750, 1000]
+    # and through the GPU kNN (run without a graph)
+    e2, _, kl2 = bh.run(c0(), bh.TsneConfig())
+    np.testing.assert_array_equal(e2.y.cpu().numpy(), e.y.cpu().numpy())
+
+
+def test_estimator_fit_transform(bh):
+    from paper_2212_11506_b200.workloads import c0
+    est = bh.BarnesHutTSNE(n_iter=300, exaggeration_iters=100)
+    y = est.fit_transform(c0()[:1024])
+    assert y.shape == (1024, 2) and np.isfinite(y).all()
+    assert est.kl_divergence_ > 0 and est.manifest_["kl"] == est.kl_divergence_
+    assert est.timings_["tree"]["calls"] == 300
