@@ -218,7 +218,8 @@ static SymLayout sym_layout(int64_t n, int64_t k) {
     L.m = 2 * n * k;
     int bits = 1;
     while (bits < 64 && ((uint64_t)1 << bits) < (uint64_t)n * (uint64_t)n) bits++;
-    L.key_bits = bits;
+    // keys are stored as uint64; key_bits > 32 selects the 64-bit sort
+    L.key_bits = bits > 32 ? bits : 33;
     size_t off = 0;
     auto take = [&](size_t b) { size_t o = off; off += bh_align(b); return o; };
     L.keys = take(8 * L.m);
