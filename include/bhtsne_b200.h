@@ -104,14 +104,11 @@ typedef struct bh_tree_t {
     int32_t *parent;   /* node_capacity: parent node, -1 for the root */
     int32_t *node_start; /* node_capacity: first point (sorted order) */
     int32_t *leaf_end;   /* node_capacity: one past the last point (leaves) */
-    uint32_t *nkids;     /* node_capacity scratch, zero on entry and exit */
-    uint32_t *arrive;    /* node_capacity scratch, zero on entry and exit */
     int32_t *level_off;  /* max_depth + 3 entries: level l = [off[l], off[l+1]),
                             off[max_depth + 2] = number of levels */
     int32_t *order;      /* n: sorted position -> point id */
     void *sorted_codes;  /* n codes (uint32 or uint64) */
     float *ys;           /* 2n: coordinates in sorted order (quadtree.py:476) */
-    int32_t *pt_leaf;    /* n: the leaf whose first point is t, else -1 */
     int32_t *status;     /* device int32: BH_OK or BH_ERR_CAPACITY after build */
     int32_t *rank;       /* optional n: rank[order[t]] = t (NULL: skipped) */
 } bh_tree_t;

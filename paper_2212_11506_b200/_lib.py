@@ -46,10 +46,9 @@ class TreeStruct(C.Structure):
         ("code_bits", C.c_int32), ("max_depth", C.c_int32),
         ("node", C.c_void_p), ("parent", C.c_void_p),
         ("node_start", C.c_void_p), ("leaf_end", C.c_void_p),
-        ("nkids", C.c_void_p), ("arrive", C.c_void_p),
         ("level_off", C.c_void_p), ("order", C.c_void_p),
         ("sorted_codes", C.c_void_p), ("ys", C.c_void_p),
-        ("pt_leaf", C.c_void_p), ("status", C.c_void_p),
+        ("status", C.c_void_p),
         ("rank", C.c_void_p),
     ]
 

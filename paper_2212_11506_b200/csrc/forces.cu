@@ -37,8 +37,18 @@ struct RepCounts {
     int internal, leafnodes, leafpts, accepted;
 };
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Stack entry (16 B, one STS.128 / broadcast LDS.128): x = the opened
+// node's info word (first child | (children - 1) << 29), y = mask of the
+// lanes that opened it, z = side^2 of the children's cells (f32; exact
+// quartering per level), w unused.
 template <int D, bool COUNT>
-__global__ void __launch_bounds__(kRepThreads)
+__global__ void __launch_bounds__(kRepThreads, 4)
 k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
             const int32_t *__restrict__ order,
             const float2 *__restrict__ y_query,
@@ -49,21 +59,13 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
             double *__restrict__ zblock, unsigned *__restrict__ ticket,
             double *__restrict__ z_out) {
     constexpr int CAP = 3 * D + 2;
-    __shared__ uint32_t s_first[kRepWarps][CAP];
-    __shared__ uint32_t s_mask[kRepWarps][CAP];
-    __shared__ uint8_t s_meta[kRepWarps][CAP];
-    __shared__ float s_side2[D + 1];
+    __shared__ uint4 s_stack[kRepWarps][CAP];
     __shared__ double s_z[kRepWarps];
-    __shared__ bool s_last;
+    __shared__ unsigned s_done;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x <= D) {
-        // cell side at depth d: 2 * r_span / 2^d (radius halves exactly)
-        double side = ldexp(2.0 * bounds->r_span, -(int)threadIdx.x);
-        s_side2[threadIdx.x] = (float)(side * side);
-    }
+    if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-
     const int64_t t = t_begin + ((int64_t)blockIdx.x * kRepWarps + warp) * 32 + lane;
     const bool valid = t < t_end && *status == BH_OK;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
@@ -72,114 +74,97 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
     const uint32_t self = (uint32_t)t;
     double r0 = 0.0, r1 = 0.0, z = 0.0;
     RepCounts cn = {0, 0, 0, 0};
+    uint4 *stk = s_stack[warp];
 
     int sp = 0;
     if (act) {
         if (lane == 0) {
-            s_first[warp][0] = 0;
-            s_mask[warp][0] = act;
-            s_meta[warp][0] = 0;  // (count-1) | depth << 2
+            // the root "group": node 0 alone, cell side 2 * r_span
+            const double side = 2.0 * bounds->r_span;
+            stk[0] = make_uint4(0u, act, __float_as_uint((float)(side * side)), 0u);
         }
         sp = 1;
         __syncwarp();
     }
     while (sp > 0) {
-        --sp;
-        const uint32_t first = s_first[warp][sp];
-        const uint32_t mask = s_mask[warp][sp];
-        const uint32_t meta = s_meta[warp][sp];
+        const uint4 ent = stk[--sp];
         __syncwarp();
-        const int cnt = (int)(meta & 3u) + 1;
-        const int depth = (int)(meta >> 2);
-        const bool mine = (mask >> lane) & 1u;
-        const float side2 = s_side2[depth];
-        float fz = 0.f, fx = 0.f, fy = 0.f;
-        uint32_t push_mask[4], push_info[4];
+        const uint32_t first = ent.x & BH_CHILD_MASK;
+        const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
+        const bool mine = (ent.y >> lane) & 1u;
+        const float side2 = __uint_as_float(ent.z);
+        float4 rec[4];
 #pragma unroll
-        for (int c = 0; c < 4; c++) {
-            push_mask[c] = 0;
-            push_info[c] = 0;
-            if (c < cnt) {
-                const float4 rec = __ldg(&node[first + c]);
-                const uint32_t info = __float_as_uint(rec.w);
-                const uint32_t m = __float_as_uint(rec.z);
-                if (info & BH_LEAF_BIT) {
-                    const uint32_t s = info & ~BH_LEAF_BIT;
-                    if (COUNT && mine) {
-                        cn.leafnodes++;
-                        cn.leafpts += (int)m;
-                    }
-                    if (m == 1) {
-                        // single-point leaf: its com is the point itself
-                        if (mine && s != self) {
-                            float dx = yi.x - rec.x, dy = yi.y - rec.y;
-                            float k = __frcp_rn(1.0f + dx * dx + dy * dy);
-                            float k2 = k * k;
-                            fz += k;
-                            fx += k2 * dx;
-                            fy += k2 * dy;
+        for (int c = 0; c < 4; c++)
+            if (c < cnt) rec[c] = __ldg(&node[first + c]);
+        float fz = 0.f, fx = 0.f, fy = 0.f;
+        const uint32_t side2c = __float_as_uint(side2 * 0.25f);
+        // children in reverse order: each group to open is pushed at once,
+        // so the first child's subtree is popped first
+#pragma unroll
+        for (int c = 3; c >= 0; c--) {
+            if (c >= cnt) continue;  // warp-uniform
+            const float4 r = rec[c];
+            const uint32_t info = __float_as_uint(r.w);
+            const uint32_t m = __float_as_uint(r.z);
+            const float dx = yi.x - r.x, dy = yi.y - r.y;
+            const float d2 = fmaf(dx, dx, dy * dy);
+            float w;
+            if (info & BH_LEAF_BIT) {  // warp-uniform
+                const uint32_t s = info & ~BH_LEAF_BIT;
+                if (COUNT && mine) {
+                    cn.leafnodes++;
+                    cn.leafpts += (int)m;
+                }
+                if (m > 1u) {
+                    // coincident-code bucket at max depth: points loaded
+                    // once per 32 and broadcast by shuffles
+                    for (uint32_t b = 0; b < m; b += 32) {
+                        const float2 pq = (b + lane < m) ? ys[s + b + lane]
+                                                         : make_float2(0.f, 0.f);
+                        const int nb = (int)min(32u, m - b);
+                        float bz = 0.f, bx = 0.f, by = 0.f;
+                        for (int jj = 0; jj < nb; jj++) {
+                            const float px = __shfl_sync(0xffffffffu, pq.x, jj);
+                            const float py = __shfl_sync(0xffffffffu, pq.y, jj);
+                            const float ex = yi.x - px, ey = yi.y - py;
+                            const float kk = rcp_approx(1.0f + fmaf(ex, ex, ey * ey));
+                            const float ww = (mine && s + b + jj != self) ? kk : 0.f;
+                            const float ww2 = ww * kk;
+                            bz += ww;
+                            bx = fmaf(ww2, ex, bx);
+                            by = fmaf(ww2, ey, by);
                         }
-                    } else {
-                        // coincident-code bucket at max depth: warp-cooperative
-                        for (uint32_t b = 0; b < m; b += 32) {
-                            const uint32_t q = s + b + lane;
-                            float2 pq = (b + lane < m) ? ys[q] : make_float2(0.f, 0.f);
-                            const int nb = (int)min(32u, m - b);
-                            float bz = 0.f, bx = 0.f, by = 0.f;
-                            for (int jj = 0; jj < nb; jj++) {
-                                float px = __shfl_sync(0xffffffffu, pq.x, jj);
-                                float py = __shfl_sync(0xffffffffu, pq.y, jj);
-                                if (mine && s + b + jj != self) {
-                                    float dx = yi.x - px, dy = yi.y - py;
-                                    float k = __frcp_rn(1.0f + dx * dx + dy * dy);
-                                    float k2 = k * k;
-                                    bz += k;
-                                    bx += k2 * dx;
-                                    by += k2 * dy;
-                                }
-                            }
-                            z += (double)bz;
-                            r0 += (double)bx;
-                            r1 += (double)by;
-                        }
+                        z += (double)bz;
+                        r0 += (double)bx;
+                        r1 += (double)by;
                     }
-                } else {
-                    float dx = yi.x - rec.x, dy = yi.y - rec.y;
-                    float d2 = dx * dx + dy * dy;
-                    bool acc = side2 < theta2 * d2;
-                    if (COUNT && mine) {
-                        cn.internal++;
-                        cn.accepted += acc;
-                    }
-                    if (mine && acc) {
-                        float k = __frcp_rn(1.0f + d2);
-                        float mk = (float)m * k;
-                        float mk2 = mk * k;
-                        fz += mk;
-                        fx += mk2 * dx;
-                        fy += mk2 * dy;
-                    }
-                    push_mask[c] = __ballot_sync(0xffffffffu, mine && !acc);
-                    push_info[c] = info;
+                    continue;
+                }
+                // single-point leaf: direct interaction unless it is self
+                w = (mine && s != self) ? 1.f : 0.f;
+            } else {
+                const bool acc = side2 < theta2 * d2;
+                if (COUNT && mine) {
+                    cn.internal++;
+                    cn.accepted += acc;
+                }
+                w = (mine && acc) ? __uint2float_rn(m) : 0.f;
+                const unsigned need = __ballot_sync(0xffffffffu, mine && !acc);
+                if (need) {
+                    if (lane == 0) stk[sp] = make_uint4(info, need, side2c, 0u);
+                    sp++;
                 }
             }
+            const float k = rcp_approx(1.0f + d2);
+            const float wk = w * k, wk2 = wk * k;
+            fz += wk;
+            fx = fmaf(wk2, dx, fx);
+            fy = fmaf(wk2, dy, fy);
         }
         z += (double)fz;
         r0 += (double)fx;
         r1 += (double)fy;
-        // push groups in reverse so the first child is opened first
-#pragma unroll
-        for (int c = 3; c >= 0; c--) {
-            if (push_mask[c]) {
-                if (lane == 0) {
-                    s_first[warp][sp] = push_info[c] & BH_CHILD_MASK;
-                    s_mask[warp][sp] = push_mask[c];
-                    s_meta[warp][sp] = (uint8_t)(((push_info[c] >> BH_NKIDS_SHIFT) & 3u) |
-                                                 ((uint32_t)(depth + 1) << 2));
-                }
-                sp++;
-            }
-        }
         __syncwarp();
     }
 
@@ -192,31 +177,37 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
     // Z: per-CTA partial (256 points in Morton order), then one fixed-order
     // warp reduction over all CTA partials (fixed_sum) -- the same
     // reduction the multi-GPU path applies to the gathered partials, so Z is
-    // bitwise independent of the GPU count.
-    double wz = warp_sum(z);
-    if (lane == 0) s_z[warp] = wz;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    // bitwise independent of the GPU count.  No CTA-wide
+    // barrier: the last warp of the CTA to finish folds the warp partials.
+    const double wz = warp_sum(z);
+    unsigned last = 0;
+    if (lane == 0) {
+        s_z[warp] = wz;
+        __threadfence_block();
+        last = atomicAdd(&s_done, 1u) == kRepWarps - 1;
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    __threadfence_block();
+    if (lane == 0) {
         double bz = 0.0;
-        for (int w = 0; w < kRepWarps; w++) bz = __dadd_rn(bz, s_z[w]);
+        for (int w = 0; w < kRepWarps; w++)
+            bz = __dadd_rn(bz, ((volatile double *)s_z)[w]);
         zblock[blockIdx.x] = bz;
         if (z_out) {
             __threadfence();
-            s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+            last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        } else {
+            last = 0;
         }
     }
-    if (!z_out) return;
-    __syncthreads();
-    if (s_last && warp == 0) {
-        __threadfence();
-        double tot = fixed_sum(zblock, gridDim.x);
-        if (lane == 0) {
-            *z_out = tot;
-            *ticket = 0;
-        }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    __threadfence();
+    const double tot = fixed_sum(zblock, gridDim.x);
+    if (lane == 0) {
+        *z_out = tot;
+        *ticket = 0;
     }
 }
-
 // Sum of gathered per-CTA Z partials into *out (one warp, fixed order).
 __global__ void k_fixed_sum(const double *__restrict__ x, int64_t n,
                             double *__restrict__ out) {

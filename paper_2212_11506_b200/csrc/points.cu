@@ -143,14 +143,15 @@ __device__ bool last_block(unsigned *ticket) {
     return s_last;
 }
 
-// Fixed-order reduction of the per-block partials (deterministic for a
-// given n, since the grid is a function of n).
+// Fixed-order reduction of the per-block partials by the whole (last)
+// block: thread i folds partials i, i+blockDim, ... in order, then the same
+// fixed warp/block tree as block_reduce.  Deterministic for a given n (the
+// grid is a function of n).  Result valid in thread 0.
 __device__ PtPartial reduce_partials(const PtPartial *part, int nparts) {
-    PtPartial r;
     MinMax m;
     mm_init(m);
     double a = 0.0, b = 0.0;
-    for (int i = 0; i < nparts; i++) {
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
         float4 q = __ldcg(&part[i].mm);
         m.mn0 = fminf(m.mn0, q.x);
         m.mx0 = fmaxf(m.mx0, q.y);
@@ -160,11 +161,10 @@ __device__ PtPartial reduce_partials(const PtPartial *part, int nparts) {
         a = __dadd_rn(a, __ldcg(&part[i].s0));
         b = __dadd_rn(b, __ldcg(&part[i].s1));
     }
-    r.mm = make_float4(m.mn0, m.mx0, m.mn1, m.mx1);
-    r.s0 = a;
-    r.s1 = b;
-    r.bad = m.bad;
-    return r;
+    __shared__ PtPartial s_r;
+    block_reduce(m, a, b, &s_r);
+    __syncthreads();
+    return s_r;
 }
 
 __global__ void __launch_bounds__(kPtThreads)
@@ -179,8 +179,8 @@ k_bounds(const float2 *__restrict__ y, int64_t n, int code_bits,
     }
     block_reduce(m, 0.0, 0.0, &part[blockIdx.x]);
     if (!last_block(ticket)) return;
+    PtPartial r = reduce_partials(part, gridDim.x);
     if (threadIdx.x == 0) {
-        PtPartial r = reduce_partials(part, gridDim.x);
         finalize_bounds(r.mm.x, r.mm.y, r.mm.z, r.mm.w, r.bad, code_bits,
                         0.0f, 0.0f, out);
         *ticket = 0;
@@ -269,8 +269,8 @@ k_update(float2 *__restrict__ y, float2 *__restrict__ v,
     }
     block_reduce(m, s0, s1, &part[blockIdx.x]);
     if (!last_block(ticket)) return;
+    PtPartial r = reduce_partials(part, gridDim.x);
     if (threadIdx.x == 0) {
-        PtPartial r = reduce_partials(part, gridDim.x);
         // y -= f32(mean_f64(y))   (optimizer.py:220-221); rounding is
         // monotone, so min(y - m) == f32(min(y) - m): the bounds of the
         // re-centred cloud come straight from the extrema.

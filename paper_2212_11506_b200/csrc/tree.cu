@@ -14,10 +14,13 @@
 // the whole topology is one prefix count over the sorted codes:
 //   k_tree_count  per-CTA level histograms (warp ballots)
 //   k_tree_scan   one CTA: per-level scans -> CTA offsets, level_off, M
-//   k_tree_emit   per point: node ids by ballot-popc ranks, records, parents
-// and summarize is a single bottom-up pass in which the last child to finish
-// computes its parent (f64 sums in the reference's child order, so centres of
-// mass are bit-identical to the reference's).
+//   k_tree_emit   per point: node ids by ballot-popc ranks, parents, and the
+//                 complete record of every single-point leaf (its centre of
+//                 mass is the point itself: f64 sum of one value / 1)
+// Summarize then runs level by level, deepest first (the reference's own
+// schedule): a node's children are the consecutive next-level nodes whose
+// parent is the node; f64 sums in the reference's child order, so centres
+// of mass are bit-identical to the reference's.
 #include "common.cuh"
 
 namespace bh {
@@ -26,6 +29,8 @@ constexpr int kTreeThreads = 256;
 constexpr int kTreeWarps = kTreeThreads / 32;
 constexpr int kTreePPT = 8;  // sub-chunks per CTA
 constexpr int kTreeChunk = kTreeThreads * kTreePPT;
+constexpr int kSumThreads = 256;
+constexpr int kSumBlocks = kSMs * 4;
 
 template <typename K>
 __device__ __forceinline__ int same_digits(const K *__restrict__ sc, int64_t t,
@@ -117,8 +122,7 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
             const uint32_t *__restrict__ blk_off,
             const int32_t *__restrict__ level_off, float4 *__restrict__ node,
             int32_t *__restrict__ parent, int32_t *__restrict__ node_start,
-            int32_t *__restrict__ leaf_end, uint32_t *__restrict__ nkids,
-            float2 *__restrict__ ys, int32_t *__restrict__ pt_leaf,
+            int32_t *__restrict__ leaf_end, float2 *__restrict__ ys,
             int32_t *__restrict__ rank, const int32_t *__restrict__ status) {
     if (*status != BH_OK) return;
     __shared__ uint32_t s_bal[kTreeWarps][D + 1];
@@ -163,24 +167,26 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
                        __popc(s_bal[warp][d] & lt);
             };
             const int32_t pid = order[t];
-            ys[t] = y[pid];
+            const float2 p = y[pid];
+            ys[t] = p;
             if (rank) rank[pid] = (int32_t)t;
-            int32_t leaf_id = -1;
             for (int d = lo; d <= hi; d++) {
-                int32_t id = base(d);
-                bool leaf = (s1 < d) || d == D;
-                uint32_t info = leaf ? (BH_LEAF_BIT | (uint32_t)t) : (uint32_t)base(d + 1);
-                int32_t par = d == 0 ? -1 : (d == lo ? base(d - 1) - 1 : base(d - 1));
-                node[id].w = __uint_as_float(info);
-                parent[id] = par;
+                const int32_t id = base(d);
+                const bool leaf = (s1 < d) || d == D;
+                parent[id] = d == 0 ? -1 : (d == lo ? base(d - 1) - 1 : base(d - 1));
                 node_start[id] = (int32_t)t;
-                if (par >= 0) atomicAdd(&nkids[par], 1u);
-                if (leaf) {
-                    leaf_id = id;
-                    if (s1 < D) leaf_end[id] = (int32_t)(t + 1);
+                if (!leaf) {
+                    node[id].w = __uint_as_float((uint32_t)base(d + 1));
+                } else if (s1 < D) {
+                    // single-point leaf: complete record (quadtree.py:490-498)
+                    node[id] = make_float4(p.x, p.y, __uint_as_float(1u),
+                                           __uint_as_float(BH_LEAF_BIT | (uint32_t)t));
+                    leaf_end[id] = (int32_t)(t + 1);
+                } else {
+                    // first point of a run of equal codes (depth-D bucket)
+                    node[id].w = __uint_as_float(BH_LEAF_BIT | (uint32_t)t);
                 }
             }
-            pt_leaf[t] = leaf_id;
             // last point of a run of equal codes closes its depth-D leaf
             if (s0 == D && s1 < D) leaf_end[base(D) - 1] = (int32_t)(t + 1);
         }
@@ -188,66 +194,57 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
     }
 }
 
-__global__ void __launch_bounds__(256)
-k_summarize(float4 *__restrict__ node, const int32_t *__restrict__ parent,
-            const int32_t *__restrict__ leaf_end, uint32_t *__restrict__ nkids,
-            uint32_t *__restrict__ arrive, const float2 *__restrict__ ys,
-            const int32_t *__restrict__ pt_leaf, int64_t n,
-            const int32_t *__restrict__ status) {
+// Summarize one level (quadtree.py:481-508).  Internal node: children are
+// the consecutive level-(d+1) nodes with parent == node (at most 4);
+// mass = sum, com = sum(m_ch * f64(com_ch)) / m in child order.  Leaves
+// still open here are depth-D buckets: f64 mean of their points in order.
+__global__ void __launch_bounds__(kSumThreads)
+k_summarize_level(float4 *__restrict__ node, const int32_t *__restrict__ parent,
+                  const int32_t *__restrict__ leaf_end,
+                  const float2 *__restrict__ ys,
+                  const int32_t *__restrict__ level_off, int d, int D,
+                  const int32_t *__restrict__ status) {
     if (*status != BH_OK) return;
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    int32_t cur = pt_leaf[t];
-    if (cur < 0) return;
-    // leaf: f64 mean of its points in sorted order (quadtree.py:490-498)
-    int32_t end = leaf_end[cur];
-    uint32_t cnt = (uint32_t)(end - t);
-    float cx, cy;
-    if (cnt == 1) {
-        float2 p = ys[t];
-        cx = p.x;
-        cy = p.y;
-    } else {
-        double a = 0.0, b = 0.0;
-        for (int64_t q = t; q < end; q++) {
-            float2 p = ys[q];
-            a = __dadd_rn(a, (double)p.x);
-            b = __dadd_rn(b, (double)p.y);
+    const int32_t lo = level_off[d], hi = level_off[d + 1];
+    const int32_t hi_next = d < D ? level_off[d + 2] : hi;
+    for (int32_t nd = lo + blockIdx.x * kSumThreads + threadIdx.x; nd < hi;
+         nd += gridDim.x * kSumThreads) {
+        const uint32_t info = __float_as_uint(node[nd].w);
+        if (info & BH_LEAF_BIT) {
+            if (d < D) continue;  // single-point leaf, completed by emit
+            const uint32_t t = info & ~BH_LEAF_BIT;
+            const int32_t end = leaf_end[nd];
+            const uint32_t cnt = (uint32_t)end - t;
+            if (cnt == 1) continue;  // completed by emit
+            double a = 0.0, b = 0.0;
+            for (int64_t q = t; q < end; q++) {
+                const float2 p = ys[q];
+                a = __dadd_rn(a, (double)p.x);
+                b = __dadd_rn(b, (double)p.y);
+            }
+            node[nd] = make_float4(__double2float_rn(__ddiv_rn(a, (double)cnt)),
+                                   __double2float_rn(__ddiv_rn(b, (double)cnt)),
+                                   __uint_as_float(cnt), __uint_as_float(info));
+            continue;
         }
-        cx = __double2float_rn(__ddiv_rn(a, (double)cnt));
-        cy = __double2float_rn(__ddiv_rn(b, (double)cnt));
-    }
-    node[cur] = make_float4(cx, cy, __uint_as_float(cnt),
-                            __uint_as_float(BH_LEAF_BIT | (uint32_t)t));
-    // internal: mass-weighted f64 mean of the children, child order
-    // (quadtree.py:499-508); the last child to arrive computes the parent
-    while (true) {
-        int32_t p = parent[cur];
-        if (p < 0) break;
-        __threadfence();
-        uint32_t got = atomicAdd(&arrive[p], 1u) + 1;
-        // read after the arrival: only the last child can see the full
-        // count; an earlier child may see it or the last child's reset (0)
-        uint32_t k = __ldcg(&nkids[p]);
-        if (got != k) break;
-        __threadfence();
-        uint32_t fc = __float_as_uint(node[p].w) & BH_CHILD_MASK;
-        uint32_t m = 0;
+        const uint32_t fc = info & BH_CHILD_MASK;
+        uint32_t m = 0, k = 0;
         double a = 0.0, b = 0.0;
-        for (uint32_t c = 0; c < k; c++) {
-            float4 r = __ldcg(&node[fc + c]);
-            uint32_t mc = __float_as_uint(r.z);
-            m += mc;
-            a = __dadd_rn(a, __dmul_rn((double)mc, (double)r.x));
-            b = __dadd_rn(b, __dmul_rn((double)mc, (double)r.y));
+#pragma unroll
+        for (uint32_t c = 0; c < 4; c++) {
+            if ((int32_t)(fc + c) < hi_next && parent[fc + c] == nd) {
+                const float4 r = node[fc + c];
+                const uint32_t mc = __float_as_uint(r.z);
+                m += mc;
+                a = __dadd_rn(a, __dmul_rn((double)mc, (double)r.x));
+                b = __dadd_rn(b, __dmul_rn((double)mc, (double)r.y));
+                k = c + 1;
+            }
         }
-        node[p] = make_float4(__double2float_rn(__ddiv_rn(a, (double)m)),
-                              __double2float_rn(__ddiv_rn(b, (double)m)),
-                              __uint_as_float(m),
-                              __uint_as_float(fc | ((k - 1) << BH_NKIDS_SHIFT)));
-        arrive[p] = 0;
-        nkids[p] = 0;
-        cur = p;
+        node[nd] = make_float4(__double2float_rn(__ddiv_rn(a, (double)m)),
+                               __double2float_rn(__ddiv_rn(b, (double)m)),
+                               __uint_as_float(m),
+                               __uint_as_float(fc | ((k - 1) << BH_NKIDS_SHIFT)));
     }
 }
 
@@ -279,8 +276,8 @@ static int build_impl(const bh_tree_t *t, const float *y, void *ws,
     BH_CHECK_LAUNCH("k_tree_scan");
     k_tree_emit<K, D><<<L.nblk, kTreeThreads, 0, st>>>(
         sc, t->order, (const float2 *)y, t->n_points, off, t->level_off,
-        (float4 *)t->node, t->parent, t->node_start, t->leaf_end, t->nkids,
-        (float2 *)t->ys, t->pt_leaf, t->rank, t->status);
+        (float4 *)t->node, t->parent, t->node_start, t->leaf_end,
+        (float2 *)t->ys, t->rank, t->status);
     BH_CHECK_LAUNCH("k_tree_emit");
     return BH_OK;
 }
@@ -306,9 +303,14 @@ extern "C" int bh_build_tree(const bh_tree_t *t, const float *y, void *ws,
 
 extern "C" int bh_summarize(const bh_tree_t *t, bh_stream_t stream) {
     BH_REQUIRE(t && t->n_points >= 1, "need at least one point");
-    k_summarize<<<bh_blocks(t->n_points, 256), 256, 0, bh_cs(stream)>>>(
-        (float4 *)t->node, t->parent, t->leaf_end, t->nkids, t->arrive,
-        (const float2 *)t->ys, t->pt_leaf, t->n_points, t->status);
-    BH_CHECK_LAUNCH("k_summarize");
+    const int D = t->max_depth;
+    int grid = bh_blocks(t->n_points, kSumThreads);
+    if (grid > kSumBlocks) grid = kSumBlocks;
+    for (int d = D; d >= 0; d--) {
+        k_summarize_level<<<grid, kSumThreads, 0, bh_cs(stream)>>>(
+            (float4 *)t->node, t->parent, t->leaf_end, (const float2 *)t->ys,
+            t->level_off, d, D, t->status);
+        BH_CHECK_LAUNCH("k_summarize_level");
+    }
     return BH_OK;
 }

@@ -235,10 +235,10 @@ class Engine:
 
     def kernels_per_iteration(self) -> int:
         """Kernel launches of one iteration (morton, sort histogram + one
-        pass per byte, 3 tree kernels, summarize, attractive, repulsive,
-        update; + the Z-partials sum when sharded)."""
-        return 1 + 1 + self.code_bits // 8 + 3 + 1 + 1 + 1 + 1 + (
-            1 if self.shard is not None else 0)
+        pass per byte, 3 tree kernels, one summarize kernel per level,
+        attractive, repulsive, update; + the Z-partials sum when sharded)."""
+        return (1 + 1 + self.code_bits // 8 + 3 + (self.code_bits // 2 + 1)
+                + 1 + 1 + 1 + (1 if self.shard is not None else 0))
 
     def _enqueue(self, ev=None):
         st = stream()

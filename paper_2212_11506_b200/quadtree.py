@@ -135,15 +135,12 @@ class TreeArrays:
         self.parent = torch.zeros(cap, **i32)
         self.node_start = torch.zeros(cap, **i32)
         self.leaf_end = torch.zeros(cap, **i32)
-        self.nkids = torch.zeros(cap, **i32)   # zero invariant (see ABI)
-        self.arrive = torch.zeros(cap, **i32)  # zero invariant
         self.level_off = torch.zeros(self.max_depth + 3, **i32)
         self.order = torch.zeros(n, **i32)
         self.sorted_codes = torch.zeros(
             n, dtype=torch.int32 if code_bits == 32 else torch.int64,
             device=device)
         self.ys = torch.zeros((n, 2), dtype=torch.float32, device=device)
-        self.pt_leaf = torch.zeros(n, **i32)
         self.status = torch.zeros(1, **i32)
         self.ws = _lib.workspace(lib.bh_tree_workspace_bytes(n, code_bits))
         self.struct = _lib.TreeStruct(
@@ -151,11 +148,11 @@ class TreeArrays:
             max_depth=self.max_depth, node=self.node.data_ptr(),
             parent=self.parent.data_ptr(),
             node_start=self.node_start.data_ptr(),
-            leaf_end=self.leaf_end.data_ptr(), nkids=self.nkids.data_ptr(),
-            arrive=self.arrive.data_ptr(), level_off=self.level_off.data_ptr(),
+            leaf_end=self.leaf_end.data_ptr(),
+            level_off=self.level_off.data_ptr(),
             order=self.order.data_ptr(),
             sorted_codes=self.sorted_codes.data_ptr(), ys=self.ys.data_ptr(),
-            pt_leaf=self.pt_leaf.data_ptr(), status=self.status.data_ptr())
+            status=self.status.data_ptr())
 
     def sref(self):
         return C.byref(self.struct)
