@@ -248,6 +248,22 @@ int bh_pad_csr_fill(const int64_t *row_ptr, const int32_t *col,
                     const float *val, int64_t n, const int64_t *out_row_ptr,
                     int32_t *out_col, float *out_val, bh_stream_t stream);
 
+/* ---- relabeling (engine-internal locality; not a reference interface) ----
+ * The optimiser periodically renumbers points in the current Morton order so
+ * that CSR rows, their column gathers and the traversal's outputs are
+ * spatially coherent.  perm[new] = old, rank[old] = new. */
+int bh_gather_rows(const void *src, const int32_t *idx, int64_t n,
+                   int elem_bytes, void *dst, bh_stream_t stream);
+int bh_scatter_rows(const void *src, const int32_t *idx, int64_t n,
+                    int elem_bytes, void *dst, bh_stream_t stream);
+int bh_invert_perm(const int32_t *perm, int64_t n, int32_t *inv,
+                   bh_stream_t stream);
+size_t bh_permute_csr_workspace_bytes(int64_t n);
+int bh_permute_csr(const int64_t *row_ptr, const int32_t *col, const float *val,
+                   const int32_t *perm, const int32_t *rank, int64_t n,
+                   int64_t *out_row_ptr, int32_t *out_col, float *out_val,
+                   void *ws, size_t ws_bytes, bh_stream_t stream);
+
 /* ---- exact kNN (knn.py:36-73) ---------------------
  * f64 squared distances summed over columns in order, k smallest per row,
  * ties -> lower id, self excluded; distances returned as float32.

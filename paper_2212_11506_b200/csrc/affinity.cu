@@ -375,3 +375,72 @@ extern "C" int bh_pad_csr_fill(const int64_t *row_ptr, const int32_t *col,
     BH_CHECK_LAUNCH("k_pad_fill");
     return BH_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Morton relabeling of the sparse P (locality of the attractive gathers):
+// new row r = old row perm[r]; columns mapped through rank (old -> new).
+// Rows keep their padding (pad entries point at their own row).
+// ---------------------------------------------------------------------------
+namespace bh {
+
+struct PermLen {
+    const int64_t *rp;
+    const int32_t *perm;
+    __device__ int64_t operator()(int64_t r) const {
+        const int64_t o = perm[r];
+        return rp[o + 1] - rp[o];
+    }
+};
+
+__global__ void k_permute_csr_fill(const int64_t *__restrict__ rp,
+                                   const int32_t *__restrict__ col,
+                                   const float *__restrict__ val,
+                                   const int32_t *__restrict__ perm,
+                                   const int32_t *__restrict__ rank, int64_t n,
+                                   const int64_t *__restrict__ orp,
+                                   int32_t *__restrict__ ocol,
+                                   float *__restrict__ oval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = wid; r < n; r += nw) {
+        const int64_t o = perm[r], s = rp[o], len = rp[o + 1] - s, d = orp[r];
+        for (int64_t q = lane; q < len; q += 32) {
+            ocol[d + q] = rank[col[s + q]];
+            oval[d + q] = val[s + q];
+        }
+    }
+}
+
+__global__ void k_set_last(int64_t *__restrict__ out_rp, int64_t n,
+                           const int64_t *__restrict__ total) {
+    out_rp[n] = *total;
+}
+
+}  // namespace bh
+
+extern "C" size_t bh_permute_csr_workspace_bytes(int64_t n) {
+    return scan_ws<int64_t, PermLen>(n) + 256;
+}
+
+extern "C" int bh_permute_csr(const int64_t *row_ptr, const int32_t *col,
+                              const float *val, const int32_t *perm,
+                              const int32_t *rank, int64_t n,
+                              int64_t *out_row_ptr, int32_t *out_col,
+                              float *out_val, void *ws, size_t ws_bytes,
+                              bh_stream_t stream) {
+    BH_REQUIRE(ws_bytes >= bh_permute_csr_workspace_bytes(n),
+               "permute workspace too small");
+    cudaStream_t st = bh_cs(stream);
+    int64_t *total = (int64_t *)((char *)ws + scan_ws<int64_t, PermLen>(n));
+    int rc = device_scan<int64_t>(PermLen{row_ptr, perm}, n, out_row_ptr, total,
+                                  ws, st);
+    if (rc != BH_OK) return rc;
+    k_set_last<<<1, 1, 0, st>>>(out_row_ptr, n, total);
+    int grid = bh_blocks(n, 8);
+    if (grid > kSMs * 32) grid = kSMs * 32;
+    k_permute_csr_fill<<<grid, 256, 0, st>>>(row_ptr, col, val, perm, rank, n,
+                                             out_row_ptr, out_col, out_val);
+    BH_CHECK_LAUNCH("k_permute_csr_fill");
+    return BH_OK;
+}

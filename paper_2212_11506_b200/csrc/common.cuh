@@ -30,14 +30,15 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
+// GPU-scope relaxed accesses for flag+value words (decoupled look-back).
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
     uint32_t v;
-    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 
-__device__ __forceinline__ void st_volatile(uint32_t *p, uint32_t v) {
-    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
 // Block-level exclusive prefix sum of one value per thread (blockDim <= 1024,

@@ -45,15 +45,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // Stack entry (16 B, one STS.128 / broadcast LDS.128): x = the opened
 // node's info word (first child | (children - 1) << 29), y = mask of the
-// lanes that opened it, z = side^2 of the children's cells (f32; exact
-// quartering per level), w unused.
-template <int D, bool COUNT>
+// lanes that opened it, z = R2 = side^2 / theta^2 of the children's cells
+// (f32; exact quartering per level), w unused.
+template <int D, bool COUNT, bool QUERY>
 __global__ void __launch_bounds__(kRepThreads, 4)
 k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
             const int32_t *__restrict__ order,
             const float2 *__restrict__ y_query,
             const bh_bounds_t *__restrict__ bounds,
-            const int32_t *__restrict__ status, float theta2, int64_t t_begin,
+            const int32_t *__restrict__ status, double theta, int64_t t_begin,
             int64_t t_end, int sorted_out, float2 *__restrict__ rep,
             double *__restrict__ zpart, int4 *__restrict__ counts,
             double *__restrict__ zblock, unsigned *__restrict__ ticket,
@@ -79,9 +79,11 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
     int sp = 0;
     if (act) {
         if (lane == 0) {
-            // the root "group": node 0 alone, cell side 2 * r_span
+            // the root "group": node 0 alone; R2 = (2 r_span)^2 / theta^2
+            // (+inf at theta = 0: nothing is ever accepted)
             const double side = 2.0 * bounds->r_span;
-            stk[0] = make_uint4(0u, act, __float_as_uint((float)(side * side)), 0u);
+            const float r2root = (float)((side * side) / (theta * theta));
+            stk[0] = make_uint4(0u, act, __float_as_uint(r2root), 0u);
         }
         sp = 1;
         __syncwarp();
@@ -92,13 +94,13 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
         const uint32_t first = ent.x & BH_CHILD_MASK;
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const bool mine = (ent.y >> lane) & 1u;
-        const float side2 = __uint_as_float(ent.z);
+        const float r2 = __uint_as_float(ent.z);
         float4 rec[4];
 #pragma unroll
         for (int c = 0; c < 4; c++)
             if (c < cnt) rec[c] = __ldg(&node[first + c]);
         float fz = 0.f, fx = 0.f, fy = 0.f;
-        const uint32_t side2c = __float_as_uint(side2 * 0.25f);
+        const uint32_t r2c = __float_as_uint(r2 * 0.25f);
         // children in reverse order: each group to open is pushed at once,
         // so the first child's subtree is popped first
 #pragma unroll
@@ -144,7 +146,9 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
                 // single-point leaf: direct interaction unless it is self
                 w = (mine && s != self) ? 1.f : 0.f;
             } else {
-                const bool acc = side2 < theta2 * d2;
+                // accepted iff d2 > R2 (R2 = side^2 / theta^2): the
+                // reference's (2r)^2 < theta^2 d^2 (forces.py:112-116)
+                const bool acc = d2 > r2;
                 if (COUNT && mine) {
                     cn.internal++;
                     cn.accepted += acc;
@@ -152,7 +156,7 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
                 w = (mine && acc) ? __uint2float_rn(m) : 0.f;
                 const unsigned need = __ballot_sync(0xffffffffu, mine && !acc);
                 if (need) {
-                    if (lane == 0) stk[sp] = make_uint4(info, need, side2c, 0u);
+                    if (lane == 0) stk[sp] = make_uint4(info, need, r2c, 0u);
                     sp++;
                 }
             }
@@ -231,7 +235,10 @@ k_attractive(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                                     : 1.0f)
                              : exag_param;
     const int gl = threadIdx.x % G;
-    const int64_t row = row_begin + (int64_t)blockIdx.x * (256 / G) + threadIdx.x / G;
+    // rows interleaved over CTAs in 32-row batches (grid-stride)
+    for (int64_t r0 = row_begin + (int64_t)blockIdx.x * (256 / G); r0 < row_end;
+         r0 += (int64_t)gridDim.x * (256 / G)) {
+    const int64_t row = r0 + threadIdx.x / G;
     const bool ok = row < row_end;
     int64_t s = 0, e = 0;
     float2 yi = make_float2(0.f, 0.f);
@@ -251,7 +258,7 @@ k_attractive(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
 #define BH_ATTR_TERM(YJ, V)                                                   \
     {                                                                         \
         float dx = yi.x - YJ.x, dy = yi.y - YJ.y;                             \
-        float pq = __fmul_rn(V, exag) * __frcp_rn(1.0f + dx * dx + dy * dy);  \
+        float pq = __fmul_rn(V, exag) * rcp_approx(1.0f + dx * dx + dy * dy); \
         fx += pq * dx;                                                        \
         fy += pq * dy;                                                        \
     }
@@ -280,6 +287,7 @@ k_attractive(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
         a1 += __shfl_xor_sync(0xffffffffu, a1, o);
     }
     if (ok && gl == 0) attr[row] = make_float2((float)a0, (float)a1);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -416,22 +424,28 @@ extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
     char *w = (char *)ws;
     if (!zblock) zblock = (double *)w;
     unsigned *ticket = (unsigned *)(w + bh_align(sizeof(double) * grid));
-    const float theta2 = (float)(theta * theta);
     cudaStream_t st = bh_cs(stream);
-#define BH_REP_LAUNCH(D, CNT)                                                 \
-    k_repulsive<D, CNT><<<grid, kRepThreads, 0, st>>>(                        \
+#define BH_REP_LAUNCH(D, CNT, Q)                                              \
+    k_repulsive<D, CNT, Q><<<grid, kRepThreads, 0, st>>>(                     \
         (const float4 *)t->node, (const float2 *)t->ys, t->order,             \
-        (const float2 *)y_query, bounds, t->status, theta2, t_begin, t_end,   \
+        (const float2 *)y_query, bounds, t->status, theta, t_begin, t_end,    \
         sorted_out, (float2 *)rep, zpart, (int4 *)counts, zblock, ticket,     \
         z_out)
+#define BH_REP_LAUNCH2(D)                                                     \
+    if (y_query) {                                                            \
+        if (counts) BH_REP_LAUNCH(D, true, true); else BH_REP_LAUNCH(D, false, true); \
+    } else {                                                                  \
+        if (counts) BH_REP_LAUNCH(D, true, false); else BH_REP_LAUNCH(D, false, false); \
+    }
     if (t->code_bits == 32) {
-        if (counts) BH_REP_LAUNCH(16, true); else BH_REP_LAUNCH(16, false);
+        BH_REP_LAUNCH2(16)
     } else if (t->code_bits == 64) {
-        if (counts) BH_REP_LAUNCH(32, true); else BH_REP_LAUNCH(32, false);
+        BH_REP_LAUNCH2(32)
     } else {
         return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
     }
 #undef BH_REP_LAUNCH
+#undef BH_REP_LAUNCH2
     BH_CHECK_LAUNCH("k_repulsive");
     return BH_OK;
 }

@@ -372,3 +372,68 @@ extern "C" int bh_center(float *y, int64_t n, const bh_bounds_t *bounds,
     BH_CHECK_LAUNCH("k_center");
     return BH_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Row gather / scatter / permutation inverse (relabeling plumbing).
+// ---------------------------------------------------------------------------
+namespace bh {
+
+template <typename T>
+__global__ void k_gather(const T *__restrict__ src, const int32_t *__restrict__ idx,
+                         int64_t n, T *__restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+template <typename T>
+__global__ void k_scatter(const T *__restrict__ src, const int32_t *__restrict__ idx,
+                          int64_t n, T *__restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[idx[i]] = src[i];
+}
+
+__global__ void k_invert(const int32_t *__restrict__ perm, int64_t n,
+                         int32_t *__restrict__ inv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        inv[perm[i]] = (int32_t)i;
+}
+
+}  // namespace bh
+
+extern "C" int bh_gather_rows(const void *src, const int32_t *idx, int64_t n,
+                              int elem_bytes, void *dst, bh_stream_t stream) {
+    const int grid = pt_grid(n);
+    cudaStream_t st = bh_cs(stream);
+    if (elem_bytes == 4)
+        k_gather<uint32_t><<<grid, kPtThreads, 0, st>>>((const uint32_t *)src, idx, n, (uint32_t *)dst);
+    else if (elem_bytes == 8)
+        k_gather<uint2><<<grid, kPtThreads, 0, st>>>((const uint2 *)src, idx, n, (uint2 *)dst);
+    else
+        return set_error(BH_ERR_ARG, "elem_bytes must be 4 or 8");
+    BH_CHECK_LAUNCH("k_gather");
+    return BH_OK;
+}
+
+extern "C" int bh_scatter_rows(const void *src, const int32_t *idx, int64_t n,
+                               int elem_bytes, void *dst, bh_stream_t stream) {
+    const int grid = pt_grid(n);
+    cudaStream_t st = bh_cs(stream);
+    if (elem_bytes == 4)
+        k_scatter<uint32_t><<<grid, kPtThreads, 0, st>>>((const uint32_t *)src, idx, n, (uint32_t *)dst);
+    else if (elem_bytes == 8)
+        k_scatter<uint2><<<grid, kPtThreads, 0, st>>>((const uint2 *)src, idx, n, (uint2 *)dst);
+    else
+        return set_error(BH_ERR_ARG, "elem_bytes must be 4 or 8");
+    BH_CHECK_LAUNCH("k_scatter");
+    return BH_OK;
+}
+
+extern "C" int bh_invert_perm(const int32_t *perm, int64_t n, int32_t *inv,
+                              bh_stream_t stream) {
+    k_invert<<<pt_grid(n), kPtThreads, 0, bh_cs(stream)>>>(perm, n, inv);
+    BH_CHECK_LAUNCH("k_invert");
+    return BH_OK;
+}

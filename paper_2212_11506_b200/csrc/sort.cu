@@ -18,7 +18,7 @@ constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kValMask = (1u << 30) -
 
 template <typename K>
 struct SortCfg {
-    static constexpr int IPT = sizeof(K) == 4 ? 16 : 12;
+    static constexpr int IPT = sizeof(K) == 4 ? 8 : 12;
     static constexpr int TILE = kSortThreads * IPT;
     static constexpr size_t SMEM = (size_t)TILE * (sizeof(K) + 4);
     static_assert(SMEM <= 40 * 1024, "tile must fit the default smem limit");
@@ -31,11 +31,34 @@ k_sort_hist(const K *__restrict__ keys, int64_t n, int passes,
     __shared__ uint32_t sh[8][256];
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        K k = keys[i];
-        for (int p = 0; p < passes; p++)
-            atomicAdd(&sh[p][(unsigned)(k >> (8 * p)) & 0xFFu], 1u);
+    // Each thread counts a run of kRun consecutive keys with run-length
+    // aggregation: the keys arrive nearly sorted (the previous iteration's
+    // Morton order), so the high digits change rarely within a run and cost
+    // one shared atomic per change instead of one per key.
+    constexpr int kRun = 16;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * kRun; s < n;
+         s += nthreads * kRun) {
+        const int cnt = (int)min((int64_t)kRun, n - s);
+        K kk[kRun];
+#pragma unroll
+        for (int j = 0; j < kRun; j++) kk[j] = j < cnt ? keys[s + j] : K(0);
+        for (int p = 0; p < passes; p++) {
+            unsigned cur = (unsigned)(kk[0] >> (8 * p)) & 0xFFu, run = 1;
+#pragma unroll
+            for (int j = 1; j < kRun; j++) {
+                if (j >= cnt) break;
+                const unsigned d = (unsigned)(kk[j] >> (8 * p)) & 0xFFu;
+                if (d == cur) {
+                    run++;
+                } else {
+                    atomicAdd(&sh[p][cur], run);
+                    cur = d;
+                    run = 1;
+                }
+            }
+            atomicAdd(&sh[p][cur], run);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
@@ -116,19 +139,31 @@ k_sort_pass(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
     const uint32_t tile = s_tile;
     uint32_t prefix = 0;
     if (tile == 0) {
-        st_volatile(&status[d], kFlagP | cnt);
+        st_relaxed(&status[d], kFlagP | cnt);
     } else {
-        st_volatile(&status[(size_t)tile * 256 + d], kFlagA | cnt);
+        st_relaxed(&status[(size_t)tile * 256 + d], kFlagA | cnt);
+        // look back 4 predecessors per round trip; stop at the first
+        // inclusive prefix (P), re-poll from the first unpublished one
         int64_t p = (int64_t)tile - 1;
-        while (true) {
-            uint32_t w = ld_volatile(&status[(size_t)p * 256 + d]);
-            uint32_t f = w & ~kValMask;
-            if (f == 0) continue;
-            prefix += w & kValMask;
-            if (f == kFlagP) break;
-            p--;
+        bool done = false;
+        while (!done) {
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                w[k] = p - k >= 0 ? ld_relaxed(&status[(size_t)(p - k) * 256 + d]) : 0u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const uint32_t f = w[k] & ~kValMask;
+                if (f == 0) break;
+                prefix += w[k] & kValMask;
+                p--;
+                if (f == kFlagP) {
+                    done = true;
+                    break;
+                }
+            }
         }
-        st_volatile(&status[(size_t)tile * 256 + d], kFlagP | (prefix + cnt));
+        st_relaxed(&status[(size_t)tile * 256 + d], kFlagP | (prefix + cnt));
     }
     s_glob[d] += prefix;
     __syncthreads();

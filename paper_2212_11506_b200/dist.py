@@ -103,7 +103,7 @@ class Shard:
         from ._lib import call, ptr
         import ctypes as C
         r0, r1 = self.plan.mine
-        y = eng.e.y
+        y = eng.y  # storage order (see Engine.relabel)
         # attr[row] for rows [r0, r1) lands at attr_send[row - r0]
         base = C.c_void_p(self.attr_send.data_ptr() - 8 * r0)
         call("bh_attractive", ptr(eng.rp), ptr(eng.col), ptr(eng.val), eng.n,

@@ -40,7 +40,7 @@ from .quadtree import (DEFAULT_CODE_BITS, TreeArrays, as_points, build_tree,
 
 STAGES = ("knn", "bsp", "tree", "summarize", "attractive", "repulsive",
           "update")
-EXTRA_STAGES = ("comm",)
+EXTRA_STAGES = ("comm", "relabel")
 MOMENTUM_SWITCH_ITER = 250
 PRECISIONS = ("f32",)
 
@@ -62,6 +62,7 @@ class TsneConfig:
     kl_every: int = 0
     code_bits: int = DEFAULT_CODE_BITS
     graph_chunk: int = 25
+    relabel_every: int = 50  # Morton renumbering period (0: never)
 
     def validate(self) -> "TsneConfig":
         if self.perplexity <= 1:
@@ -90,6 +91,8 @@ class TsneConfig:
             raise ValueError(f"code_bits must be 32 or 64, got {self.code_bits}")
         if self.graph_chunk < 1:
             raise ValueError("graph_chunk must be >= 1")
+        if self.relabel_every < 0:
+            raise ValueError("relabel_every must be >= 0")
         return self
 
     @property
@@ -181,12 +184,22 @@ def embedding_from(y, v=None, g=None, iteration=0) -> Embedding:
                      g=torch.ones_like(pts) if g is None else as_points(g).clone(),
                      iteration=iteration)
 
-
 # ---------------------------------------------------------------------------
-# Engine: all buffers of the loop preallocated; one iteration = 8 launches
-# (+ 3 sort passes) enqueued on the current stream; graph-captured.
+# Engine: every buffer of the loop preallocated in HBM; one iteration = one
+# Morton pass, the radix-sort passes, 3 tree kernels, one summarize kernel
+# per level, attractive, repulsive and update, enqueued on the current
+# stream and captured in CUDA graphs.  The state is kept in a private
+# "storage order" that is periodically renumbered to the current Morton
+# order (relabel): CSR rows, their column gathers, the traversal's reads and
+# writes then touch nearby memory.  Results are returned in point-id order.
 # ---------------------------------------------------------------------------
 class Engine:
+    # events: 0 start | 1 tree built | 2 summarized | 3 attractive |
+    #         4 repulsive | 5 exchange done (multi-GPU) | 6 updated
+    N_EVENTS = 7
+    STAGE_EVENTS = {"tree": (0, 1), "summarize": (1, 2), "attractive": (2, 3),
+                    "repulsive": (3, 4), "update": (5, 6)}
+
     def __init__(self, p: SparseAffinity, e: Embedding, cfg: TsneConfig,
                  schedule: bool = True, shard=None):
         lib = _lib.load()
@@ -197,9 +210,15 @@ class Engine:
         self.code_bits = cfg.code_bits
         dev = e.y.device
         self.dev = dev
-        self.rp, self.col, self.val = p.padded()
-        self.attr = torch.zeros((n, 2), dtype=torch.float32, device=dev)
-        self.rep = torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        f2 = lambda: torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        i32 = lambda: torch.zeros(n, dtype=torch.int32, device=dev)
+        # storage-order state (ids[s] = point id stored at slot s)
+        self.y, self.v, self.g, self.tmp = f2(), f2(), f2(), f2()
+        self.ids = torch.arange(n, dtype=torch.int32, device=dev)
+        self.ids_tmp, self.rank = i32(), i32()
+        self.csr = {"p": p.padded()}
+        self.csr_key = "p"
+        self.attr, self.rep = f2(), f2()
         exag_on = schedule and cfg.n_iter > 0 and cfg.exaggeration_iters > 0
         self.sched = _lib.struct_tensor(SCHED_DTYPE, dict(
             iteration=e.iteration,
@@ -219,19 +238,27 @@ class Engine:
         self.ws_rep = _lib.workspace(lib.bh_repulsive_workspace_bytes(n))
         self.ws_upd = _lib.workspace(lib.bh_update_workspace_bytes(n))
         self.ws_bnd = _lib.workspace(lib.bh_bounds_workspace_bytes(n))
+        self.ws_perm = None
         self.z_dev = self.sched[48:56].view(torch.float64)  # sched.z
         self.theta = float(cfg.theta)
+        self.relabel_every = cfg.relabel_every if schedule else 0
+        self.since_relabel = 0
         self.graphs = {}
         self.shard = shard
         if shard is not None:
             shard.attach(self)
 
-    # -- one iteration -----------------------------------------------------
-    # events: 0 start | 1 tree built | 2 summarized | 3 attractive |
-    #         4 repulsive | 5 exchange done (multi-GPU) | 6 updated
-    N_EVENTS = 7
-    STAGE_EVENTS = {"tree": (0, 1), "summarize": (1, 2), "attractive": (2, 3),
-                    "repulsive": (3, 4), "update": (5, 6)}
+    @property
+    def rp(self):
+        return self.csr[self.csr_key][0]
+
+    @property
+    def col(self):
+        return self.csr[self.csr_key][1]
+
+    @property
+    def val(self):
+        return self.csr[self.csr_key][2]
 
     def kernels_per_iteration(self) -> int:
         """Kernel launches of one iteration (morton, sort histogram + one
@@ -240,10 +267,11 @@ class Engine:
         return (1 + 1 + self.code_bits // 8 + 3 + (self.code_bits // 2 + 1)
                 + 1 + 1 + 1 + (1 if self.shard is not None else 0))
 
+    # -- one iteration -----------------------------------------------------
     def _enqueue(self, ev=None):
         st = stream()
         n, cb, t = self.n, self.code_bits, self.tree
-        y = self.e.y
+        y = self.y
         rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
         rec(0)
         call("bh_morton", ptr(y), n, ptr(self.bounds), cb, 1, ptr(self.codes), st)
@@ -265,7 +293,7 @@ class Engine:
             rep, rep_rank = self.rep, None
         else:
             rep, rep_rank = self.shard.forces(self, rec, st)
-        call("bh_update", ptr(y), ptr(self.e.v), ptr(self.e.g), ptr(self.attr),
+        call("bh_update", ptr(y), ptr(self.v), ptr(self.g), ptr(self.attr),
              ptr(rep), ptr(rep_rank), n, ptr(self.sched), ptr(self.bounds), cb,
              ptr(self.ws_upd), self.ws_upd.numel(), st)
         rec(6)
@@ -275,24 +303,68 @@ class Engine:
                  for _ in range(self.N_EVENTS)] for _ in range(k)]
 
     def _graph(self, k):
-        if k not in self.graphs:
+        key = (k, self.csr_key)
+        if key not in self.graphs:
             evs = self._events(k)
             g = torch.cuda.CUDAGraph()
             # the loop keeps no allocator state: capture straight away
             with torch.cuda.graph(g):
                 for i in range(k):
                     self._enqueue(evs[i])
-            self.graphs[k] = (g, evs)
-        return self.graphs[k]
+            self.graphs[key] = (g, evs)
+        return self.graphs[key]
 
+    # -- storage order -----------------------------------------------------
+    def _rows(self, name, src, idx, dst, nbytes=8):
+        call(name, ptr(src), ptr(idx), self.n, nbytes, ptr(dst), stream())
+
+    def load(self):
+        """Point-id order (Embedding) -> storage order."""
+        e = self.e
+        for src, dst in ((e.y, self.y), (e.v, self.v), (e.g, self.g)):
+            self._rows("bh_gather_rows", src, self.ids, dst)
+
+    def store(self):
+        """Storage order -> point-id order (Embedding)."""
+        e = self.e
+        for src, dst in ((self.y, e.y), (self.v, e.v), (self.g, e.g)):
+            self._rows("bh_scatter_rows", src, self.ids, dst)
+
+    def relabel(self):
+        """Renumber the storage slots in the last tree's Morton order."""
+        st = stream()
+        order = self.tree.order
+        call("bh_invert_perm", ptr(order), self.n, ptr(self.rank), st)
+        for buf in (self.y, self.v, self.g):
+            self._rows("bh_gather_rows", buf, order, self.tmp)
+            buf.copy_(self.tmp)
+        self._rows("bh_gather_rows", self.ids, order, self.ids_tmp, 4)
+        self.ids.copy_(self.ids_tmp)
+        nxt = "A" if self.csr_key != "A" else "B"
+        if nxt not in self.csr:
+            rp, col, val = self.csr["p"]
+            self.csr[nxt] = (torch.empty_like(rp), torch.empty_like(col),
+                             torch.empty_like(val))
+            if self.ws_perm is None:
+                self.ws_perm = _lib.workspace(
+                    _lib.load().bh_permute_csr_workspace_bytes(self.n))
+        rp, col, val = self.csr[self.csr_key]
+        orp, ocol, oval = self.csr[nxt]
+        call("bh_permute_csr", ptr(rp), ptr(col), ptr(val), ptr(order),
+             ptr(self.rank), self.n, ptr(orp), ptr(ocol), ptr(oval),
+             ptr(self.ws_perm), self.ws_perm.numel(), st)
+        self.csr_key = nxt
+        self.since_relabel = 0
+
+    # -- driver --------------------------------------------------------------
     def begin(self):
         """Bounds of the current (centred) Y, shift 0."""
-        call("bh_bounds", ptr(self.e.y), self.n, self.code_bits,
+        call("bh_bounds", ptr(self.y), self.n, self.code_bits,
              ptr(self.bounds), ptr(self.ws_bnd), self.ws_bnd.numel(), stream())
 
     def end(self):
         """Apply the pending re-centering of the last update."""
-        call("bh_center", ptr(self.e.y), self.n, ptr(self.bounds), stream())
+        call("bh_center", ptr(self.y), self.n, ptr(self.bounds), stream())
 
     def set_iteration(self, it: int, exaggeration: float | None = None):
         """Host override of the schedule (stage API: p carries the factor)."""
@@ -308,7 +380,9 @@ class Engine:
         s = _lib.read_struct(self.sched, SCHED_DTYPE)
         if int(s["bad"]) != INT64_MAX:
             bad = int(s["bad"])
-            raise ValueError(f"non-finite gradient at point {bad & 0xFFFFFFFF} "
+            slot = bad & 0xFFFFFFFF
+            point = int(self.ids[slot].item())
+            raise ValueError(f"non-finite gradient at point {point} "
                              f"(iteration {bad >> 32})")
         if int(self.tree.status.item()) != 0:
             raise RuntimeError("quadtree node capacity exceeded")
@@ -316,9 +390,10 @@ class Engine:
 
     def run(self, n_iter: int, timings: StepTimings | None = None,
             use_graph: bool = True):
-        """Advance n_iter iterations; Y is centred on return."""
+        """Advance n_iter iterations; the Embedding is centred on return."""
         if n_iter <= 0:
             return
+        self.load()
         self.begin()
         done = 0
         chunk = self.cfg.graph_chunk
@@ -331,6 +406,16 @@ class Engine:
                 evs = self._events(k)
                 for i in range(k):
                     self._enqueue(evs[i])
+            done += k
+            self.since_relabel += k
+            relabel = (self.relabel_every and done < n_iter
+                       and self.since_relabel >= self.relabel_every)
+            if relabel:
+                r0 = torch.cuda.Event(enable_timing=True)
+                r1 = torch.cuda.Event(enable_timing=True)
+                r0.record()
+                self.relabel()
+                r1.record()
             evs[-1][-1].synchronize()
             self._check()
             if timings is not None:
@@ -339,8 +424,11 @@ class Engine:
                         timings.add(name, evs[i][a].elapsed_time(evs[i][b]) * 1e-3)
                     if self.shard is not None:
                         timings.add("comm", evs[i][4].elapsed_time(evs[i][5]) * 1e-3)
-            done += k
+                if relabel:
+                    r1.synchronize()
+                    timings.add("relabel", r0.elapsed_time(r1) * 1e-3)
         self.end()
+        self.store()
         self.e.iteration += n_iter
 
     @property
