@@ -466,17 +466,33 @@ extern "C" int bh_attractive(const int64_t *row_ptr, const int32_t *col,
     BH_REQUIRE(row_begin >= 0 && row_end <= n_rows && row_begin <= row_end,
                "bad row range");
     if (row_end == row_begin) return BH_OK;
-    constexpr int G = 8;
-    const int grid = bh_blocks(row_end - row_begin, 256 / G);
+    // lanes per row (tuning knob BH_ATTR_G; default 16, measured best at C3:
+    // tools/microbench.py, profiles/r01_microbench.txt)
+    static const int g_env = [] {
+        const char *s = getenv("BH_ATTR_G");
+        int g = s ? atoi(s) : 16;
+        return (g == 4 || g == 8 || g == 16 || g == 32) ? g : 16;
+    }();
     cudaStream_t st = bh_cs(stream);
-    if (padded)
-        k_attractive<G, true><<<grid, 256, 0, st>>>(
-            row_ptr, col, val, (const float2 *)y, row_begin, row_end,
-            exaggeration, sched, (float2 *)attr);
-    else
-        k_attractive<G, false><<<grid, 256, 0, st>>>(
-            row_ptr, col, val, (const float2 *)y, row_begin, row_end,
-            exaggeration, sched, (float2 *)attr);
+#define BH_ATTR(G)                                                            \
+    {                                                                         \
+        const int grid = bh_blocks(row_end - row_begin, 256 / G);             \
+        if (padded)                                                           \
+            k_attractive<G, true><<<grid, 256, 0, st>>>(                      \
+                row_ptr, col, val, (const float2 *)y, row_begin, row_end,     \
+                exaggeration, sched, (float2 *)attr);                         \
+        else                                                                  \
+            k_attractive<G, false><<<grid, 256, 0, st>>>(                     \
+                row_ptr, col, val, (const float2 *)y, row_begin, row_end,     \
+                exaggeration, sched, (float2 *)attr);                         \
+    }
+    switch (g_env) {
+        case 4: BH_ATTR(4) break;
+        case 8: BH_ATTR(8) break;
+        case 32: BH_ATTR(32) break;
+        default: BH_ATTR(16) break;
+    }
+#undef BH_ATTR
     BH_CHECK_LAUNCH("k_attractive");
     return BH_OK;
 }

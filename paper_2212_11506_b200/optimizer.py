@@ -194,11 +194,15 @@ def embedding_from(y, v=None, g=None, iteration=0) -> Embedding:
 # writes then touch nearby memory.  Results are returned in point-id order.
 # ---------------------------------------------------------------------------
 class Engine:
-    # events: 0 start | 1 tree built | 2 summarized | 3 attractive |
-    #         4 repulsive | 5 exchange done (multi-GPU) | 6 updated
-    N_EVENTS = 7
-    STAGE_EVENTS = {"tree": (0, 1), "summarize": (1, 2), "attractive": (2, 3),
-                    "repulsive": (3, 4), "update": (5, 6)}
+    # events: 0 start | 1 tree built | 2 summarized | 3 attractive done |
+    #         4 repulsive done | 5 forces joined / exchanged | 6 updated |
+    #         7 attractive start (side stream)
+    N_EVENTS = 8
+    STAGE_EVENTS = {"tree": (0, 1), "summarize": (1, 2), "attractive": (7, 3),
+                    "repulsive": (2, 4), "update": (5, 6)}
+    STAGE_EVENTS_SHARDED = {"tree": (0, 1), "summarize": (1, 2),
+                            "attractive": (2, 3), "repulsive": (3, 4),
+                            "update": (5, 6)}
 
     def __init__(self, p: SparseAffinity, e: Embedding, cfg: TsneConfig,
                  schedule: bool = True, shard=None):
@@ -244,6 +248,14 @@ class Engine:
         self.relabel_every = cfg.relabel_every if schedule else 0
         self.since_relabel = 0
         self.graphs = {}
+        # the iteration chain runs (and is captured) on a high-priority
+        # stream; the CSR sweep on a low-priority side stream fills the SMs
+        # the latency-bound chain leaves idle
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.main = torch.cuda.Stream(device=dev, priority=hi)
+        self.side = torch.cuda.Stream(device=dev, priority=lo)
+        self.fork_ev = torch.cuda.Event()
+        self.join_ev = torch.cuda.Event()
         self.shard = shard
         if shard is not None:
             shard.attach(self)
@@ -275,6 +287,20 @@ class Engine:
         rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
         rec(0)
         call("bh_morton", ptr(y), n, ptr(self.bounds), cb, 1, ptr(self.codes), st)
+        if self.shard is None:
+            # fork: the memory-bound CSR sweep needs only the centred Y, so
+            # it runs on a side stream under the latency-bound sort / tree /
+            # summarize chain and the issue-bound traversal
+            main = torch.cuda.current_stream()
+            self.fork_ev.record(main)
+            with torch.cuda.stream(self.side):
+                self.side.wait_event(self.fork_ev)
+                rec(7)
+                call("bh_attractive", ptr(self.rp), ptr(self.col), ptr(self.val),
+                     n, 1, ptr(y), 0, n, 1.0, ptr(self.sched), ptr(self.attr),
+                     stream())
+                rec(3)
+                self.join_ev.record(self.side)
         call("bh_sort", ptr(self.codes), n, cb, ptr(t.sorted_codes),
              ptr(t.order), ptr(self.ws_sort), self.ws_sort.numel(), st)
         t.build(y, st)
@@ -282,13 +308,11 @@ class Engine:
         t.summarize(st)
         rec(2)
         if self.shard is None:
-            call("bh_attractive", ptr(self.rp), ptr(self.col), ptr(self.val), n,
-                 1, ptr(y), 0, n, 1.0, ptr(self.sched), ptr(self.attr), st)
-            rec(3)
             call("bh_repulsive", t.sref(), ptr(self.bounds), self.theta, None,
                  0, n, 0, ptr(self.rep), None, None, ptr(self.z_dev), None,
                  ptr(self.ws_rep), self.ws_rep.numel(), st)
             rec(4)
+            torch.cuda.current_stream().wait_event(self.join_ev)
             rec(5)
             rep, rep_rank = self.rep, None
         else:
@@ -308,7 +332,7 @@ class Engine:
             evs = self._events(k)
             g = torch.cuda.CUDAGraph()
             # the loop keeps no allocator state: capture straight away
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=self.main):
                 for i in range(k):
                     self._enqueue(evs[i])
             self.graphs[key] = (g, evs)
@@ -390,9 +414,17 @@ class Engine:
 
     def run(self, n_iter: int, timings: StepTimings | None = None,
             use_graph: bool = True):
-        """Advance n_iter iterations; the Embedding is centred on return."""
+        """Advance n_iter iterations; the Embedding is centred on return.
+        Work is stream-ordered after (and before) the caller's stream."""
         if n_iter <= 0:
             return
+        caller = torch.cuda.current_stream()
+        self.main.wait_stream(caller)
+        with torch.cuda.stream(self.main):
+            self._run(n_iter, timings, use_graph)
+        caller.wait_stream(self.main)
+
+    def _run(self, n_iter, timings, use_graph):
         self.load()
         self.begin()
         done = 0
@@ -420,7 +452,9 @@ class Engine:
             self._check()
             if timings is not None:
                 for i in range(k):
-                    for name, (a, b) in self.STAGE_EVENTS.items():
+                    stages = (self.STAGE_EVENTS if self.shard is None
+                              else self.STAGE_EVENTS_SHARDED)
+                    for name, (a, b) in stages.items():
                         timings.add(name, evs[i][a].elapsed_time(evs[i][b]) * 1e-3)
                     if self.shard is not None:
                         timings.add("comm", evs[i][4].elapsed_time(evs[i][5]) * 1e-3)

@@ -1,0 +1,115 @@
+"""Kernel microbenchmarks on late-iteration C3 state (GPU; tuning aid).
+
+    python tools/microbench.py [--preroll 600] [--reps 20]
+
+Advances the C3 problem (bench.py setup cache) to a late iteration, then
+times the attractive sweep and the BH traversal in isolation with CUDA
+events for each value of the environment knobs given on the command line
+(each run in a fresh subprocess so the library re-reads the knob).
+Prints one JSON line per configuration.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+
+def child(args):
+    import numpy as np
+    import torch
+
+    import bench
+    import paper_2212_11506_b200 as bh
+    from paper_2212_11506_b200._lib import call, ptr, stream
+
+    dev = torch.device("cuda", 0)
+    prob = bench.problem(args.config, dev)
+    p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
+    cache = f"/tmp/bh_bench_cache/{args.config}_y{args.preroll}.npy"
+    cfg = bh.TsneConfig(theta=args.theta)
+    if os.path.exists(cache):
+        y = np.load(cache)
+        e = bh.embedding_from(y)
+        e.iteration = args.preroll
+    else:
+        e = bh.embedding_from(prob["y0"])
+        eng = bh.Engine(p, e, cfg)
+        eng.run(args.preroll)
+        np.save(cache, e.y.cpu().numpy())
+    eng = bh.Engine(p, e, cfg)
+    t = eng.tree
+    st = stream()
+
+    def build():
+        call("bh_morton", ptr(eng.y), eng.n, ptr(eng.bounds), 32, 0,
+             ptr(eng.codes), st)
+        call("bh_sort", ptr(eng.codes), eng.n, 32, ptr(t.sorted_codes),
+             ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st)
+        t.build(eng.y)
+        t.summarize()
+
+    eng.load()
+    eng.begin()
+    build()
+    eng.relabel()  # storage (Y and P) in Morton order, as in the engine
+    eng.begin()
+    build()
+    torch.cuda.synchronize()
+
+    def timeit(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    att = lambda: call("bh_attractive", ptr(eng.rp), ptr(eng.col), ptr(eng.val),
+                       eng.n, 1, ptr(eng.y), 0, eng.n, 1.0, None, ptr(eng.attr), st)
+    rep = lambda: call("bh_repulsive", t.sref(), ptr(eng.bounds), float(args.theta),
+                       None, 0, eng.n, 0, ptr(eng.rep), None, None, ptr(eng.z_dev),
+                       None, ptr(eng.ws_rep), eng.ws_rep.numel(), st)
+    out = {"knobs": {k: v for k, v in os.environ.items() if k.startswith("BH_")},
+           "iteration": args.preroll,
+           "attractive_ms": timeit(att, args.reps),
+           "repulsive_ms": timeit(rep, args.reps)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--preroll", type=int, default=600)
+    ap.add_argument("--theta", type=float, default=0.5)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--child", action="store_true")
+    ap.add_argument("--sweep", nargs="*", default=[],
+                    help="NAME=v1,v2,... environment knobs to sweep")
+    args = ap.parse_args()
+    if args.child:
+        return child(args)
+    combos = [{}]
+    for s in args.sweep:
+        name, vals = s.split("=")
+        combos = [dict(c, **{name: v}) for c in combos for v in vals.split(",")]
+    for c in combos:
+        env = dict(os.environ, **c)
+        cmd = [sys.executable, __file__, "--child", "--config", args.config,
+               "--preroll", str(args.preroll), "--theta", str(args.theta),
+               "--reps", str(args.reps)]
+        subprocess.run(cmd, env=env, check=False)
+
+
+if __name__ == "__main__":
+    main()
