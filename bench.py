@@ -1,7 +1,11 @@
 """Benchmark: BH t-SNE gradient iterations/sec at N=1.3M (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c3|c2|c1|c0] [--preroll R]
+                    [--config c3|c2|c1|c0|c4] [--preroll R]
+
+Defaults (no flags): N=1, W=5, K=995 -- the timed region is the rest of the
+full 1000-iteration run (about 2-3 s of GPU time plus ~1 min of setup).
+--config c4 runs the per-kernel microbench of BASELINE.json configs[4].
 
 A step is one gradient iteration (tree build, summarize, attractive,
 repulsive, update) of the full N=1.3M, D=50, K=90 problem (config C3,
@@ -425,14 +429,140 @@ def e2e_host(bh, p, cfg, y_host, args):
                    "D2H; host wall clock", "steps": steps}
 
 
+def c4_problem(dev, n=4_000_000, k=90, seed=0):
+    """BASELINE.json configs[4]: 2-D points from 100 Student-t (nu=2)
+    clusters; random symmetric P with k distinct neighbours != i per row,
+    values U(0,1]+1e-3 row-normalised, then symmetrised (affinity.py:121).
+    The random graph is drawn with torch on the device (setup); the
+    symmetrisation is our bh_symmetrize."""
+    import torch
+
+    import paper_2212_11506_b200 as bh
+    from paper_2212_11506_b200 import workloads
+    from paper_2212_11506_b200.affinity import PerplexityResult
+    y = workloads.c4_points(seed, n)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed + 1)
+    idx = torch.empty((n, k), dtype=torch.int64, device=dev)
+    chunk = 1 << 20
+    rows_all = torch.arange(n, device=dev)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        rows = rows_all[s:e, None]
+        cand = torch.randint(0, n - 1, (e - s, k), generator=g, device=dev)
+        cand = cand + (cand >= rows).to(torch.int64)
+        for _ in range(20):  # redraw duplicated entries until rows are distinct
+            srt, order = torch.sort(cand, dim=1)
+            dup = torch.zeros_like(cand, dtype=torch.bool)
+            dup[:, 1:] = srt[:, 1:] == srt[:, :-1]
+            if not bool(dup.any()):
+                break
+            redraw = torch.randint(0, n - 1, srt.shape, generator=g, device=dev)
+            redraw = redraw + (redraw >= rows).to(torch.int64)
+            cand = torch.where(dup, redraw, srt)
+        idx[s:e] = cand
+    vals = 1.0 - torch.rand((n, k), generator=g, device=dev, dtype=torch.float64)
+    vals = vals + 1e-3
+    vals = vals / vals.sum(dim=1, keepdim=True)
+    graph = bh.NeighborGraph(idx, torch.ones((n, k), device=dev))
+    pr = PerplexityResult(betas=torch.ones(n, dtype=torch.float64, device=dev),
+                          conditional=vals)
+    p = bh.symmetrize(pr, graph)
+    return y, p
+
+
+def c4_arm(args, rank, world):
+    """Per-kernel microbench (no optimiser): attractive CSR sweep and the BH
+    traversal at theta in {0.2, 0.5, 0.8}, GB/s of algorithmic bytes vs the
+    measured HBM peak; sharded over ranks like the engine."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2212_11506_b200 as bh
+    from paper_2212_11506_b200 import _lib
+    from paper_2212_11506_b200._lib import call, ptr, stream
+    from paper_2212_11506_b200.dist import ShardPlan
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    y, p = c4_problem(dev)
+    torch.cuda.synchronize()
+    log(f"[setup] c4 N={y.shape[0]} nnz={p.nnz} in {time.time() - t0:.1f}s")
+    n, nnz = y.shape[0], p.nnz
+    plan = ShardPlan(n, world, rank)
+    lo, hi = plan.mine
+    yt = torch.from_numpy(y).to(dev)
+    c, r = bh.compute_bounds(yt)
+    tree = bh.summarize(bh.build_tree(bh.morton_codes(yt, c, r), yt))
+    rp, col, val = p.padded()
+    attr = torch.empty((n, 2), dtype=torch.float32, device=dev)
+    rep = torch.empty((n, 2), dtype=torch.float32, device=dev)
+    ws = _lib.workspace(_lib.load().bh_repulsive_workspace_bytes(n))
+    zt = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b) / reps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    try:
+        peak = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        peak = FALLBACK_HBM_GBS
+    kernels = {}
+    ms = timed(lambda: call("bh_attractive", ptr(rp), ptr(col), ptr(val), n, 1,
+                            ptr(yt), lo, hi, 1.0, None, ptr(attr), stream()),
+               max(3, args.steps))
+    b = 8.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    kernels["attractive"] = {"ms": ms, "algorithmic_bytes": b,
+                             "achieved_gbs": b / ms / 1e6, "frac": b / ms / 1e6 / peak}
+    for theta in (0.2, 0.5, 0.8):
+        fn = lambda: call("bh_repulsive", tree.arrays.sref(), ptr(tree.bounds),
+                          theta, None, lo, hi, 0, ptr(rep), None, None, ptr(zt),
+                          None, ptr(ws), ws.numel(), stream())
+        ms = timed(fn, max(2, args.steps // 4))
+        cnt = bh.repulsive_counts(tree, theta).astype(np.int64).sum(axis=0)
+        b = 16.0 * (cnt[0] + cnt[1]) + 8.0 * cnt[2] + 28.0 * n
+        kernels[f"repulsive_theta{theta}"] = {
+            "ms": ms, "algorithmic_bytes": b, "achieved_gbs": b / ms / 1e6,
+            "frac": b / ms / 1e6 / peak, "visits_per_point": (cnt[0] + cnt[1]) / n,
+            "leaf_points_per_point": cnt[2] / n}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "C4 kernel microbench: per-kernel GB/s of algorithmic "
+                      "bytes vs measured HBM peak", "n_gpus": world,
+            "config": {"workload": "c4: N=4M 2-D Student-t(2) mixture of 100 "
+                                   "clusters, random symmetric P (K=90)",
+                       "n_points": n, "nnz": nnz, "code_bits": 32},
+            "peak_gbs": peak, "kernels": kernels,
+            "data": "synthetic (BASELINE.json configs[4])"}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=995)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--preroll", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c0", "c1", "c2", "c3"])
+    ap.add_argument("--config", default="c3",
+                    choices=["c0", "c1", "c2", "c3", "c4"])
     ap.add_argument("--theta", type=float, default=0.5)
     ap.add_argument("--chunk", type=int, default=25)
     ap.add_argument("--cpu-steps", type=int, default=2)
@@ -450,7 +580,15 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
     try:
-        if args.impl == "reference":
+        if args.config == "c4":
+            if args.impl == "reference":
+                if rank == 0:
+                    print(json.dumps({"impl": "reference", "unavailable":
+                                      "c4 is a GPU kernel microbench; the CPU "
+                                      "oracle is reported on c3"}))
+            else:
+                c4_arm(args, rank, world)
+        elif args.impl == "reference":
             reference_arm(args, rank, world)
         else:
             ours_arm(args, rank, world)

@@ -360,3 +360,31 @@ def test_estimator_fit_transform(bh):
     assert y.shape == (1024, 2) and np.isfinite(y).all()
     assert est.kl_divergence_ > 0 and est.manifest_["kl"] == est.kl_divergence_
     assert est.timings_["tree"]["calls"] == 300
+
+
+def test_sharded_engine_single_rank_matches_unsharded(bh):
+    """The multi-GPU code path (Shard: row/position ranges, sorted-order
+    forces, NCCL all-gathers, Z partials) on a 1-rank NCCL group must give
+    the bitwise-identical trajectory of the unsharded engine."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2212_11506_b200.dist import Shard
+    a = golden("affinity450")
+    p = bh.from_csr(a["row_offsets"], a["col_indices"], a["values"])
+    cfg = bh.TsneConfig(n_iter=80, exaggeration_iters=30, graph_chunk=10)
+    e1 = bh.init_embedding(450, seed=3)
+    bh.Engine(p, e1, cfg).run(80)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        e2 = bh.init_embedding(450, seed=3)
+        bh.Engine(p, e2, cfg, shard=Shard(0, 1)).run(80)
+    finally:
+        dist.destroy_process_group()
+    np.testing.assert_array_equal(e2.y.cpu().numpy(), e1.y.cpu().numpy())
