@@ -151,7 +151,10 @@ int bh_build_tree(const bh_tree_t *tree, const float *y, void *ws,
 /* ---- summarize (quadtree.py:481-519) --------------------------------------
  * Bottom-up centre of mass and count; bit-identical to the reference
  * (f64 sums in reference order, stored as float32). */
-int bh_summarize(const bh_tree_t *tree, bh_stream_t stream);
+int bh_summarize(const bh_tree_t *tree, void *ws, size_t ws_bytes,
+                 bh_stream_t stream);
+/* ws: the bh_tree_workspace_bytes() workspace (holds a grid barrier; all
+ * levels run in one cooperative launch when the device supports it). */
 
 /* ---- attractive force (forces.py:56-82) ---------------------------------
  * attr[i] = sum_t v_t*(y_i - y_j)/(1+|y_i-y_j|^2) over CSR row i, for rows

@@ -43,6 +43,123 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+struct Acc64 {
+    double z, r0, r1;
+};
+
+// Per-pop context of a lane: its point, the group's R2 and whether the lane
+// opened the node whose children are being visited.
+struct GroupCtx {
+    const float4 *__restrict__ node;
+    const float2 *__restrict__ ys;
+    float2 yi;
+    float r2;
+    bool mine;
+    uint32_t self;
+    int lane;
+};
+
+// One child for one lane (the reference rule, forces.py:99-128).  Returns
+// the ballot of lanes that must open it (0 for leaves); the lane's f32
+// contribution goes to (fz, fx, fy), a bucket leaf's straight into a64.
+template <bool COUNT>
+__device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
+                                             float &fz, float &fx, float &fy,
+                                             Acc64 &a64, RepCounts &cn) {
+    const uint32_t info = __float_as_uint(r.w);
+    const uint32_t m = __float_as_uint(r.z);
+    const float dx = g.yi.x - r.x, dy = g.yi.y - r.y;
+    const float d2 = fmaf(dx, dx, dy * dy);
+    float w;
+    uint32_t need = 0;
+    if (info & BH_LEAF_BIT) {  // warp-uniform
+        const uint32_t s = info & ~BH_LEAF_BIT;
+        if (COUNT && g.mine) {
+            cn.leafnodes++;
+            cn.leafpts += (int)m;
+        }
+        if (m > 1u) {
+            // coincident-code bucket at max depth (warp-uniform, rare):
+            // points loaded once per 32 and broadcast by shuffles
+            for (uint32_t b = 0; b < m; b += 32) {
+                const float2 pq = (b + g.lane < m) ? g.ys[s + b + g.lane]
+                                                   : make_float2(0.f, 0.f);
+                const int nb = (int)min(32u, m - b);
+                float bz = 0.f, bx = 0.f, by = 0.f;
+                for (int jj = 0; jj < nb; jj++) {
+                    const float px = __shfl_sync(0xffffffffu, pq.x, jj);
+                    const float py = __shfl_sync(0xffffffffu, pq.y, jj);
+                    const float ex = g.yi.x - px, ey = g.yi.y - py;
+                    const float kk = rcp_approx(1.0f + fmaf(ex, ex, ey * ey));
+                    const float ww = (g.mine && s + b + jj != g.self) ? kk : 0.f;
+                    const float ww2 = ww * kk;
+                    bz += ww;
+                    bx = fmaf(ww2, ex, bx);
+                    by = fmaf(ww2, ey, by);
+                }
+                a64.z += (double)bz;
+                a64.r0 += (double)bx;
+                a64.r1 += (double)by;
+            }
+            return 0;
+        }
+        // single-point leaf: direct interaction unless it is self
+        w = (g.mine && s != g.self) ? 1.f : 0.f;
+    } else {
+        // accepted iff d2 > R2 (R2 = side^2 / theta^2): the reference's
+        // (2r)^2 < theta^2 d^2 (forces.py:112-116)
+        const bool acc = d2 > g.r2;
+        if (COUNT && g.mine) {
+            cn.internal++;
+            cn.accepted += acc;
+        }
+        w = (g.mine && acc) ? __uint2float_rn(m) : 0.f;
+        need = __ballot_sync(0xffffffffu, g.mine && !acc);
+    }
+    const float k = rcp_approx(1.0f + d2);
+    const float wk = w * k, wk2 = wk * k;
+    fz += wk;
+    fx = fmaf(wk2, dx, fx);
+    fy = fmaf(wk2, dy, fy);
+    return need;
+}
+
+// Visit the CNT consecutive children starting at `first`, then push every
+// child some lane must open in one lane-parallel step (lane c writes child
+// c's entry; child 0 ends on top so the first subtree is popped first).
+template <int CNT, bool COUNT>
+__device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
+                                         Acc64 &a64, RepCounts &cn,
+                                         uint4 *stk, int &sp) {
+    float4 rec[CNT];
+#pragma unroll
+    for (int c = 0; c < CNT; c++) rec[c] = __ldg(&g.node[first + c]);
+    float fz = 0.f, fx = 0.f, fy = 0.f;
+    uint32_t pm[CNT];
+#pragma unroll
+    for (int c = 0; c < CNT; c++) pm[c] = bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
+    a64.z += (double)fz;
+    a64.r0 += (double)fx;
+    a64.r1 += (double)fy;
+    uint32_t nz = 0;
+#pragma unroll
+    for (int c = 0; c < CNT; c++) nz |= (pm[c] != 0u ? 1u : 0u) << c;
+    if (nz) {
+        if (g.lane < CNT && ((nz >> g.lane) & 1u)) {
+            uint32_t info = __float_as_uint(rec[0].w), msk = pm[0];
+#pragma unroll
+            for (int c = 1; c < CNT; c++)
+                if (g.lane == c) {
+                    info = __float_as_uint(rec[c].w);
+                    msk = pm[c];
+                }
+            stk[sp + __popc(nz >> (g.lane + 1))] =
+                make_uint4(info, msk, __float_as_uint(g.r2 * 0.25f), 0u);
+        }
+        sp += __popc(nz);
+    }
+}
+
 // Stack entry (16 B, one STS.128 / broadcast LDS.128): x = the opened
 // node's info word (first child | (children - 1) << 29), y = mask of the
 // lanes that opened it, z = R2 = side^2 / theta^2 of the children's cells
@@ -95,80 +212,18 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const bool mine = (ent.y >> lane) & 1u;
         const float r2 = __uint_as_float(ent.z);
-        float4 rec[4];
-#pragma unroll
-        for (int c = 0; c < 4; c++)
-            if (c < cnt) rec[c] = __ldg(&node[first + c]);
-        float fz = 0.f, fx = 0.f, fy = 0.f;
-        const uint32_t r2c = __float_as_uint(r2 * 0.25f);
-        // children in reverse order: each group to open is pushed at once,
-        // so the first child's subtree is popped first
-#pragma unroll
-        for (int c = 3; c >= 0; c--) {
-            if (c >= cnt) continue;  // warp-uniform
-            const float4 r = rec[c];
-            const uint32_t info = __float_as_uint(r.w);
-            const uint32_t m = __float_as_uint(r.z);
-            const float dx = yi.x - r.x, dy = yi.y - r.y;
-            const float d2 = fmaf(dx, dx, dy * dy);
-            float w;
-            if (info & BH_LEAF_BIT) {  // warp-uniform
-                const uint32_t s = info & ~BH_LEAF_BIT;
-                if (COUNT && mine) {
-                    cn.leafnodes++;
-                    cn.leafpts += (int)m;
-                }
-                if (m > 1u) {
-                    // coincident-code bucket at max depth: points loaded
-                    // once per 32 and broadcast by shuffles
-                    for (uint32_t b = 0; b < m; b += 32) {
-                        const float2 pq = (b + lane < m) ? ys[s + b + lane]
-                                                         : make_float2(0.f, 0.f);
-                        const int nb = (int)min(32u, m - b);
-                        float bz = 0.f, bx = 0.f, by = 0.f;
-                        for (int jj = 0; jj < nb; jj++) {
-                            const float px = __shfl_sync(0xffffffffu, pq.x, jj);
-                            const float py = __shfl_sync(0xffffffffu, pq.y, jj);
-                            const float ex = yi.x - px, ey = yi.y - py;
-                            const float kk = rcp_approx(1.0f + fmaf(ex, ex, ey * ey));
-                            const float ww = (mine && s + b + jj != self) ? kk : 0.f;
-                            const float ww2 = ww * kk;
-                            bz += ww;
-                            bx = fmaf(ww2, ex, bx);
-                            by = fmaf(ww2, ey, by);
-                        }
-                        z += (double)bz;
-                        r0 += (double)bx;
-                        r1 += (double)by;
-                    }
-                    continue;
-                }
-                // single-point leaf: direct interaction unless it is self
-                w = (mine && s != self) ? 1.f : 0.f;
-            } else {
-                // accepted iff d2 > R2 (R2 = side^2 / theta^2): the
-                // reference's (2r)^2 < theta^2 d^2 (forces.py:112-116)
-                const bool acc = d2 > r2;
-                if (COUNT && mine) {
-                    cn.internal++;
-                    cn.accepted += acc;
-                }
-                w = (mine && acc) ? __uint2float_rn(m) : 0.f;
-                const unsigned need = __ballot_sync(0xffffffffu, mine && !acc);
-                if (need) {
-                    if (lane == 0) stk[sp] = make_uint4(info, need, r2c, 0u);
-                    sp++;
-                }
-            }
-            const float k = rcp_approx(1.0f + d2);
-            const float wk = w * k, wk2 = wk * k;
-            fz += wk;
-            fx = fmaf(wk2, dx, fx);
-            fy = fmaf(wk2, dy, fy);
+        const GroupCtx g{node, ys, yi, r2, mine, self, lane};
+        Acc64 a{z, r0, r1};
+        // straight-line code for the (warp-uniform) number of children
+        switch (cnt) {
+            case 1: bh_group<1, COUNT>(g, first, a, cn, stk, sp); break;
+            case 2: bh_group<2, COUNT>(g, first, a, cn, stk, sp); break;
+            case 3: bh_group<3, COUNT>(g, first, a, cn, stk, sp); break;
+            default: bh_group<4, COUNT>(g, first, a, cn, stk, sp); break;
         }
-        z += (double)fz;
-        r0 += (double)fx;
-        r1 += (double)fy;
+        z = a.z;
+        r0 = a.r0;
+        r1 = a.r1;
         __syncwarp();
     }
 

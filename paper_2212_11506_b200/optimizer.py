@@ -203,6 +203,14 @@ class Engine:
     STAGE_EVENTS_SHARDED = {"tree": (0, 1), "summarize": (1, 2),
                             "attractive": (2, 3), "repulsive": (3, 4),
                             "update": (5, 6)}
+    STAGE_EVENTS_SEQ = {"tree": (0, 1), "summarize": (1, 2),
+                        "attractive": (7, 3), "repulsive": (3, 4),
+                        "update": (5, 6)}
+
+    def _stage_events(self):
+        if self.shard is not None:
+            return self.STAGE_EVENTS_SHARDED
+        return self.STAGE_EVENTS if self.overlap else self.STAGE_EVENTS_SEQ
 
     def __init__(self, p: SparseAffinity, e: Embedding, cfg: TsneConfig,
                  schedule: bool = True, shard=None):
@@ -254,6 +262,10 @@ class Engine:
         lo, hi = torch.cuda.Stream.priority_range()
         self.main = torch.cuda.Stream(device=dev, priority=hi)
         self.side = torch.cuda.Stream(device=dev, priority=lo)
+        # True: the CSR sweep runs on the side stream under the chain
+        # (measured +0.6% at C3, profiles/README.md); off by default so the
+        # cooperative summarize launch never contends for SM slots
+        self.overlap = False
         self.fork_ev = torch.cuda.Event()
         self.join_ev = torch.cuda.Event()
         self.shard = shard
@@ -276,7 +288,7 @@ class Engine:
         """Kernel launches of one iteration (morton, sort histogram + one
         pass per byte, 3 tree kernels, one summarize kernel per level,
         attractive, repulsive, update; + the Z-partials sum when sharded)."""
-        return (1 + 1 + self.code_bits // 8 + 3 + (self.code_bits // 2 + 1)
+        return (1 + 1 + self.code_bits // 8 + 3 + 1
                 + 1 + 1 + 1 + (1 if self.shard is not None else 0))
 
     # -- one iteration -----------------------------------------------------
@@ -287,7 +299,7 @@ class Engine:
         rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
         rec(0)
         call("bh_morton", ptr(y), n, ptr(self.bounds), cb, 1, ptr(self.codes), st)
-        if self.shard is None:
+        if self.shard is None and self.overlap:
             # fork: the memory-bound CSR sweep needs only the centred Y, so
             # it runs on a side stream under the latency-bound sort / tree /
             # summarize chain and the issue-bound traversal
@@ -308,11 +320,17 @@ class Engine:
         t.summarize(st)
         rec(2)
         if self.shard is None:
+            if not self.overlap:  # isolated kernels (stage breakdown)
+                rec(7)
+                call("bh_attractive", ptr(self.rp), ptr(self.col), ptr(self.val),
+                     n, 1, ptr(y), 0, n, 1.0, ptr(self.sched), ptr(self.attr), st)
+                rec(3)
             call("bh_repulsive", t.sref(), ptr(self.bounds), self.theta, None,
                  0, n, 0, ptr(self.rep), None, None, ptr(self.z_dev), None,
                  ptr(self.ws_rep), self.ws_rep.numel(), st)
             rec(4)
-            torch.cuda.current_stream().wait_event(self.join_ev)
+            if self.overlap:
+                torch.cuda.current_stream().wait_event(self.join_ev)
             rec(5)
             rep, rep_rank = self.rep, None
         else:
@@ -327,7 +345,7 @@ class Engine:
                  for _ in range(self.N_EVENTS)] for _ in range(k)]
 
     def _graph(self, k):
-        key = (k, self.csr_key)
+        key = (k, self.csr_key, self.overlap)
         if key not in self.graphs:
             evs = self._events(k)
             g = torch.cuda.CUDAGraph()
@@ -337,6 +355,42 @@ class Engine:
                     self._enqueue(evs[i])
             self.graphs[key] = (g, evs)
         return self.graphs[key]
+
+    def _graph1(self):
+        """One iteration without timing events (the fast path: replayed
+        back to back, the host only syncs at chunk boundaries)."""
+        key = ("fast", self.csr_key, self.overlap)
+        if key not in self.graphs:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.main):
+                self._enqueue(None)
+            self.graphs[key] = g
+        return self.graphs[key]
+
+    def _alloc_relabel(self):
+        if "A" not in self.csr:
+            rp, col, val = self.csr["p"]
+            for key in ("A", "B"):
+                self.csr[key] = (torch.empty_like(rp), torch.empty_like(col),
+                                 torch.empty_like(val))
+            self.ws_perm = _lib.workspace(
+                _lib.load().bh_permute_csr_workspace_bytes(self.n))
+
+    def prepare(self, timings: bool = False):
+        """Capture every graph a run can need (all CSR buffers), so that no
+        capture happens inside a timed region."""
+        keys = ["p"] + (["A", "B"] if self.relabel_every else [])
+        if self.relabel_every:
+            self._alloc_relabel()
+        cur = self.csr_key
+        with torch.cuda.stream(self.main):
+            for key in keys:
+                self.csr_key = key
+                self._graph1()
+                if timings:
+                    self._graph(self.cfg.graph_chunk)
+        self.csr_key = cur
+        torch.cuda.synchronize()
 
     # -- storage order -----------------------------------------------------
     def _rows(self, name, src, idx, dst, nbytes=8):
@@ -365,13 +419,7 @@ class Engine:
         self._rows("bh_gather_rows", self.ids, order, self.ids_tmp, 4)
         self.ids.copy_(self.ids_tmp)
         nxt = "A" if self.csr_key != "A" else "B"
-        if nxt not in self.csr:
-            rp, col, val = self.csr["p"]
-            self.csr[nxt] = (torch.empty_like(rp), torch.empty_like(col),
-                             torch.empty_like(val))
-            if self.ws_perm is None:
-                self.ws_perm = _lib.workspace(
-                    _lib.load().bh_permute_csr_workspace_bytes(self.n))
+        self._alloc_relabel()
         rp, col, val = self.csr[self.csr_key]
         orp, ocol, oval = self.csr[nxt]
         call("bh_permute_csr", ptr(rp), ptr(col), ptr(val), ptr(order),
@@ -431,13 +479,18 @@ class Engine:
         chunk = self.cfg.graph_chunk
         while done < n_iter:
             k = min(chunk, n_iter - done)
-            if use_graph:
+            evs = None
+            if use_graph and timings is None:
+                g = self._graph1()
+                for _ in range(k):
+                    g.replay()
+            elif use_graph:
                 g, evs = self._graph(k)
                 g.replay()
             else:
-                evs = self._events(k)
+                evs = self._events(k) if timings is not None else None
                 for i in range(k):
-                    self._enqueue(evs[i])
+                    self._enqueue(evs[i] if evs else None)
             done += k
             self.since_relabel += k
             relabel = (self.relabel_every and done < n_iter
@@ -448,13 +501,11 @@ class Engine:
                 r0.record()
                 self.relabel()
                 r1.record()
-            evs[-1][-1].synchronize()
+            self.main.synchronize()
             self._check()
             if timings is not None:
                 for i in range(k):
-                    stages = (self.STAGE_EVENTS if self.shard is None
-                              else self.STAGE_EVENTS_SHARDED)
-                    for name, (a, b) in stages.items():
+                    for name, (a, b) in self._stage_events().items():
                         timings.add(name, evs[i][a].elapsed_time(evs[i][b]) * 1e-3)
                     if self.shard is not None:
                         timings.add("comm", evs[i][4].elapsed_time(evs[i][5]) * 1e-3)

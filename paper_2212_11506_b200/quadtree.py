@@ -162,7 +162,8 @@ class TreeArrays:
              self.ws.numel(), st or stream())
 
     def summarize(self, st=None):
-        call("bh_summarize", self.sref(), st or stream())
+        call("bh_summarize", self.sref(), ptr(self.ws), self.ws.numel(),
+             st or stream())
 
 
 class MortonQuadtree:

@@ -80,10 +80,17 @@ def child(args):
     rep = lambda: call("bh_repulsive", t.sref(), ptr(eng.bounds), float(args.theta),
                        None, 0, eng.n, 0, ptr(eng.rep), None, None, ptr(eng.z_dev),
                        None, ptr(eng.ws_rep), eng.ws_rep.numel(), st)
+    def sort_build():
+        call("bh_sort", ptr(eng.codes), eng.n, 32, ptr(t.sorted_codes),
+             ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st)
+        t.build(eng.y)
+
     out = {"knobs": {k: v for k, v in os.environ.items() if k.startswith("BH_")},
            "iteration": args.preroll,
            "attractive_ms": timeit(att, args.reps),
-           "repulsive_ms": timeit(rep, args.reps)}
+           "repulsive_ms": timeit(rep, args.reps),
+           "sort_build_ms": timeit(sort_build, args.reps),
+           "summarize_ms": timeit(lambda: t.summarize(), args.reps)}
     print(json.dumps(out), flush=True)
 
 
