@@ -43,6 +43,20 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+__device__ __forceinline__ int4 ld_stream_i4(const int32_t *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ float4 ld_stream_f4(const float *p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+
 struct Acc64 {
     double z, r0, r1;
 };
@@ -305,8 +319,10 @@ k_attractive(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
     double a0 = 0.0, a1 = 0.0;
     if (PADDED) {
         for (int64_t q = s + 4 * gl; q < e; q += 4 * G) {
-            const int4 c = __ldcs(reinterpret_cast<const int4 *>(col + q));
-            const float4 v = __ldcs(reinterpret_cast<const float4 *>(val + q));
+            // the CSR stream bypasses L1 (no allocation) so that L1 holds the
+            // y_j gathers
+            const int4 c = ld_stream_i4(col + q);
+            const float4 v = ld_stream_f4(val + q);
             const float2 y0 = __ldg(&y[c.x]), y1 = __ldg(&y[c.y]);
             const float2 y2 = __ldg(&y[c.z]), y3 = __ldg(&y[c.w]);
             float fx = 0.f, fy = 0.f;
