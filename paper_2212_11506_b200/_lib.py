@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbhtsne_b200.so")
+# BH_LIB overrides the library path (A/B builds in tools/microbench.py)
+LIB_PATH = os.environ.get("BH_LIB") or os.path.join(HERE, "libbhtsne_b200.so")
 
 _lib = None
 
