@@ -157,13 +157,16 @@ template <int CNT, bool COUNT>
 __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
                                          Acc64 &a64, RepCounts &cn,
                                          uint4 *stk, int &sp) {
-    float4 rec[CNT];
+    float4 rec[CNT];  // all loads issued up front (ILP)
 #pragma unroll
     for (int c = 0; c < CNT; c++) rec[c] = __ldg(&g.node[first + c]);
     float fz = 0.f, fx = 0.f, fy = 0.f;
-    uint32_t pm[CNT];
+    uint32_t pm[CNT], inf[CNT];
 #pragma unroll
-    for (int c = 0; c < CNT; c++) pm[c] = bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
+    for (int c = 0; c < CNT; c++) {
+        inf[c] = __float_as_uint(rec[c].w);
+        pm[c] = bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
+    }
     a64.z += (double)fz;
     a64.r0 += (double)fx;
     a64.r1 += (double)fy;
@@ -172,11 +175,11 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
     for (int c = 0; c < CNT; c++) nz |= (pm[c] != 0u ? 1u : 0u) << c;
     if (nz) {
         if (g.lane < CNT && ((nz >> g.lane) & 1u)) {
-            uint32_t info = __float_as_uint(rec[0].w), msk = pm[0];
+            uint32_t info = inf[0], msk = pm[0];
 #pragma unroll
             for (int c = 1; c < CNT; c++)
                 if (g.lane == c) {
-                    info = __float_as_uint(rec[c].w);
+                    info = inf[c];
                     msk = pm[c];
                 }
             stk[sp + __popc(nz >> (g.lane + 1))] =
