@@ -15,6 +15,12 @@ namespace bh {
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kValMask = (1u << 30) - 1;
+#ifndef BH_SORT_LOOKBACK
+// predecessors polled per round trip: 4 measured best at C3 (16: +7%,
+// 32: +2x; the pass is bound by per-tile latency over ~2 waves of tiles)
+#define BH_SORT_LOOKBACK 4
+#endif
+constexpr int kLookback = BH_SORT_LOOKBACK;
 
 template <typename K>
 struct SortCfg {
@@ -142,17 +148,18 @@ k_sort_pass(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
         st_relaxed(&status[d], kFlagP | cnt);
     } else {
         st_relaxed(&status[(size_t)tile * 256 + d], kFlagA | cnt);
-        // look back 4 predecessors per round trip; stop at the first
+        // look back kLookback predecessors per L2 round trip (the P frontier
+        // then advances kLookback tiles per trip); stop at the first
         // inclusive prefix (P), re-poll from the first unpublished one
         int64_t p = (int64_t)tile - 1;
         bool done = false;
         while (!done) {
-            uint32_t w[4];
+            uint32_t w[kLookback];
 #pragma unroll
-            for (int k = 0; k < 4; k++)
+            for (int k = 0; k < kLookback; k++)
                 w[k] = p - k >= 0 ? ld_relaxed(&status[(size_t)(p - k) * 256 + d]) : 0u;
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
+            for (int k = 0; k < kLookback; k++) {
                 const uint32_t f = w[k] & ~kValMask;
                 if (f == 0) break;
                 prefix += w[k] & kValMask;
