@@ -185,6 +185,20 @@ int bh_repulsive(const bh_tree_t *tree, const bh_bounds_t *bounds,
                  int64_t t_end, int sorted_out, float *rep, double *zpart,
                  double *zblock, double *z_out, int32_t *counts, void *ws,
                  size_t ws_bytes, bh_stream_t stream);
+/* Both force passes of one iteration in ONE launch (forces.py:56-150 as
+ * called by gradient_step, optimizer.py:101-104): bh_attractive over rows
+ * [row_begin, row_end) and bh_repulsive over sorted positions
+ * [t_begin, t_end) (no query points, zpart or counts), their CTAs
+ * interleaved so the issue-bound traversal and the memory-bound CSR sweep
+ * share every SM.  Results, including Z, are bitwise those of the two
+ * separate calls.  ws: bh_repulsive_workspace_bytes(t_end - t_begin). */
+int bh_forces(const bh_tree_t *tree, const bh_bounds_t *bounds, double theta,
+              int64_t t_begin, int64_t t_end, int sorted_out, float *rep,
+              double *zblock, double *z_out, void *ws, size_t ws_bytes,
+              const int64_t *row_ptr, const int32_t *col, const float *val,
+              int64_t n_rows, int padded, const float *y, int64_t row_begin,
+              int64_t row_end, float exaggeration, const bh_sched_t *sched,
+              float *attr, bh_stream_t stream);
 /* *out = fixed-order sum of n per-CTA Z partials (see bh_repulsive). */
 int bh_sum_partials(const double *x, int64_t n, double *out,
                     bh_stream_t stream);

@@ -76,6 +76,9 @@ SIGNATURES = {
     "bh_repulsive_workspace_bytes": ([_I64], _SZ),
     "bh_repulsive": ([C.POINTER(TreeStruct), _P, C.c_double, _P, _I64, _I64,
                       C.c_int, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_forces": ([C.POINTER(TreeStruct), _P, C.c_double, _I64, _I64, C.c_int,
+                   _P, _P, _P, _P, _SZ, _P, _P, _P, _I64, C.c_int, _P, _I64,
+                   _I64, C.c_float, _P, _P, _P], C.c_int),
     "bh_sum_partials": ([_P, _I64, _P, _P], C.c_int),
     "bh_repulsive_exact_workspace_bytes": ([_I64], _SZ),
     "bh_repulsive_exact": ([_P, _I64, _P, _P, _P, _P, _SZ, _P], C.c_int),

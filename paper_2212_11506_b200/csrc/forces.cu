@@ -1,6 +1,8 @@
 // Force kernels: Barnes-Hut repulsion (forces.py:85-150), attractive CSR
 // sweep (forces.py:56-82), exact O(N^2) repulsion (forces.py:153-182) and
 // the KL rows (optimizer.py:227-239).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bh {
@@ -193,35 +195,55 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
 // node's info word (first child | (children - 1) << 29), y = mask of the
 // lanes that opened it, z = R2 = side^2 / theta^2 of the children's cells
 // (f32; exact quartering per level), w unused.
-template <int D, bool COUNT, bool QUERY>
+struct RepArgs {
+    const float4 *__restrict__ node;
+    const float2 *__restrict__ ys;
+    const int32_t *__restrict__ order;
+    const float2 *__restrict__ y_query;
+    const bh_bounds_t *__restrict__ bounds;
+    const int32_t *__restrict__ status;
+    double theta;
+    int64_t t_begin, t_end;
+    int sorted_out;
+    float2 *__restrict__ rep;
+    double *__restrict__ zpart;
+    int4 *__restrict__ counts;
+    double *__restrict__ zblock;
+    unsigned *__restrict__ ticket;
+    double *__restrict__ z_out;
+};
+
 #ifndef BH_REP_MIN_BLOCKS
 // 5 CTAs x 8 warps per SM (48 registers): measured 1.23 ms vs 1.33 ms (4),
 // 1.44 ms (3), 2.29 ms (6, heavy spills) at C3 iteration 600
 #define BH_REP_MIN_BLOCKS 5
 #endif
-__global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
-k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
-            const int32_t *__restrict__ order,
-            const float2 *__restrict__ y_query,
-            const bh_bounds_t *__restrict__ bounds,
-            const int32_t *__restrict__ status, double theta, int64_t t_begin,
-            int64_t t_end, int sorted_out, float2 *__restrict__ rep,
-            double *__restrict__ zpart, int4 *__restrict__ counts,
-            double *__restrict__ zblock, unsigned *__restrict__ ticket,
-            double *__restrict__ z_out) {
+
+// CTA `bid` of the `nblk` traversal CTAs: points t_begin + 256 bid + [0, 256).
+template <int D, bool COUNT, bool QUERY>
+__device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
+                                          int64_t nblk) {
     constexpr int CAP = 3 * D + 2;
     __shared__ uint4 s_stack[kRepWarps][CAP];
     __shared__ double s_z[kRepWarps];
     __shared__ unsigned s_done;
+    const float4 *__restrict__ node = A.node;
+    const float2 *__restrict__ ys = A.ys;
+    const int32_t *__restrict__ order = A.order;
+    const int32_t *__restrict__ status = A.status;
+    const bh_bounds_t *__restrict__ bounds = A.bounds;
+    const int64_t t_begin = A.t_begin, t_end = A.t_end;
+    const double theta = A.theta;
+    double *__restrict__ zblock = A.zblock;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-    const int64_t t = t_begin + ((int64_t)blockIdx.x * kRepWarps + warp) * 32 + lane;
+    const int64_t t = t_begin + (bid * kRepWarps + warp) * 32 + lane;
     const bool valid = t < t_end && *status == BH_OK;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     float2 yi = make_float2(0.f, 0.f);
-    if (valid) yi = y_query ? y_query[order[t]] : ys[t];
+    if (valid) yi = QUERY ? A.y_query[order[t]] : ys[t];
     const uint32_t self = (uint32_t)t;
     double r0 = 0.0, r1 = 0.0, z = 0.0;
     RepCounts cn = {0, 0, 0, 0};
@@ -262,10 +284,10 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
     }
 
     if (valid) {
-        const int64_t o = sorted_out ? t - t_begin : (int64_t)order[t];
-        rep[o] = make_float2((float)r0, (float)r1);
-        if (zpart) zpart[o] = z;
-        if (COUNT) counts[o] = make_int4(cn.internal, cn.leafnodes, cn.leafpts, cn.accepted);
+        const int64_t o = A.sorted_out ? t - t_begin : (int64_t)order[t];
+        A.rep[o] = make_float2((float)r0, (float)r1);
+        if (A.zpart) A.zpart[o] = z;
+        if (COUNT) A.counts[o] = make_int4(cn.internal, cn.leafnodes, cn.leafpts, cn.accepted);
     }
     // Z: per-CTA partial (256 points in Morton order), then one fixed-order
     // warp reduction over all CTA partials (fixed_sum) -- the same
@@ -285,21 +307,27 @@ k_repulsive(const float4 *__restrict__ node, const float2 *__restrict__ ys,
         double bz = 0.0;
         for (int w = 0; w < kRepWarps; w++)
             bz = __dadd_rn(bz, ((volatile double *)s_z)[w]);
-        zblock[blockIdx.x] = bz;
-        if (z_out) {
+        zblock[bid] = bz;
+        if (A.z_out) {
             __threadfence();
-            last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+            last = atomicAdd(A.ticket, 1u) == (unsigned)(nblk - 1);
         } else {
             last = 0;
         }
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
     __threadfence();
-    const double tot = fixed_sum(zblock, gridDim.x);
+    const double tot = fixed_sum(zblock, nblk);
     if (lane == 0) {
-        *z_out = tot;
-        *ticket = 0;
+        *A.z_out = tot;
+        *A.ticket = 0;
     }
+}
+
+template <int D, bool COUNT, bool QUERY>
+__global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
+k_repulsive(const RepArgs A) {
+    rep_block<D, COUNT, QUERY>(A, blockIdx.x, gridDim.x);
 }
 // Sum of gathered per-CTA Z partials into *out (one warp, fixed order).
 __global__ void k_fixed_sum(const double *__restrict__ x, int64_t n,
@@ -313,20 +341,35 @@ __global__ void k_fixed_sum(const double *__restrict__ x, int64_t n,
 // multiple of 4 entries so each lane issues 128-bit loads of 4 column ids
 // and 4 values (pad entries have value 0 and contribute exactly 0).
 // ---------------------------------------------------------------------------
+struct AttArgs {
+    const int64_t *__restrict__ rp;
+    const int32_t *__restrict__ col;
+    const float *__restrict__ val;
+    const float2 *__restrict__ y;
+    int64_t row_begin, row_end;
+    float exag_param;
+    const bh_sched_t *__restrict__ sched;
+    float2 *__restrict__ attr;
+};
+
+// CTA `bid` of `nblk` sweeping CTAs (256 threads): row batches of 256 / G
+// rows, batch b handled by CTA b mod nblk.
 template <int G, bool PADDED>
-__global__ void __launch_bounds__(256)
-k_attractive(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-             const float *__restrict__ val, const float2 *__restrict__ y,
-             int64_t row_begin, int64_t row_end, float exag_param,
-             const bh_sched_t *__restrict__ sched, float2 *__restrict__ attr) {
+__device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
+                                          int64_t nblk) {
+    const int64_t *__restrict__ rp = A.rp;
+    const int32_t *__restrict__ col = A.col;
+    const float *__restrict__ val = A.val;
+    const float2 *__restrict__ y = A.y;
+    const int64_t row_end = A.row_end;
+    const bh_sched_t *__restrict__ sched = A.sched;
     const float exag = sched ? (sched->iteration < sched->exaggeration_iters
                                     ? sched->exaggeration
                                     : 1.0f)
-                             : exag_param;
+                             : A.exag_param;
     const int gl = threadIdx.x % G;
-    // rows interleaved over CTAs in 32-row batches (grid-stride)
-    for (int64_t r0 = row_begin + (int64_t)blockIdx.x * (256 / G); r0 < row_end;
-         r0 += (int64_t)gridDim.x * (256 / G)) {
+    for (int64_t r0 = A.row_begin + bid * (256 / G); r0 < row_end;
+         r0 += nblk * (256 / G)) {
     const int64_t row = r0 + threadIdx.x / G;
     const bool ok = row < row_end;
     int64_t s = 0, e = 0;
@@ -377,8 +420,32 @@ k_attractive(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
         a0 += __shfl_xor_sync(0xffffffffu, a0, o);
         a1 += __shfl_xor_sync(0xffffffffu, a1, o);
     }
-    if (ok && gl == 0) attr[row] = make_float2((float)a0, (float)a1);
+    if (ok && gl == 0) A.attr[row] = make_float2((float)a0, (float)a1);
     }
+}
+
+template <int G, bool PADDED>
+__global__ void __launch_bounds__(256) k_attractive(const AttArgs A) {
+    att_block<G, PADDED>(A, blockIdx.x, gridDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// Fused force pass: the traversal CTAs (issue-bound) and the CSR-sweep CTAs
+// (L1/latency-bound) of one iteration in ONE grid, their block indices
+// interleaved (na of every nr + na consecutive CTAs sweep) so that both kinds
+// are co-resident on every SM and overlap, instead of running back to back.
+// Each CTA computes exactly what it computes in its own kernel; the Z
+// partials are indexed by traversal CTA, so Z is bitwise the same.
+// ---------------------------------------------------------------------------
+template <int D, int G, bool PADDED>
+__global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
+k_forces(const RepArgs R, const AttArgs A, int64_t nr, int64_t na) {
+    const int64_t b = blockIdx.x, nb = nr + na;
+    const int64_t before = (b * na) / nb, upto = ((b + 1) * na) / nb;
+    if (upto > before)
+        att_block<G, PADDED>(A, before, na);
+    else
+        rep_block<D, false, false>(R, b - upto, nr);
 }
 
 // ---------------------------------------------------------------------------
@@ -516,12 +583,11 @@ extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
     if (!zblock) zblock = (double *)w;
     unsigned *ticket = (unsigned *)(w + bh_align(sizeof(double) * grid));
     cudaStream_t st = bh_cs(stream);
-#define BH_REP_LAUNCH(D, CNT, Q)                                              \
-    k_repulsive<D, CNT, Q><<<grid, kRepThreads, 0, st>>>(                     \
-        (const float4 *)t->node, (const float2 *)t->ys, t->order,             \
-        (const float2 *)y_query, bounds, t->status, theta, t_begin, t_end,    \
-        sorted_out, (float2 *)rep, zpart, (int4 *)counts, zblock, ticket,     \
-        z_out)
+    const RepArgs A{(const float4 *)t->node, (const float2 *)t->ys, t->order,
+                    (const float2 *)y_query, bounds, t->status, theta, t_begin,
+                    t_end, sorted_out, (float2 *)rep, zpart, (int4 *)counts,
+                    zblock, ticket, z_out};
+#define BH_REP_LAUNCH(D, CNT, Q) k_repulsive<D, CNT, Q><<<grid, kRepThreads, 0, st>>>(A)
 #define BH_REP_LAUNCH2(D)                                                     \
     if (y_query) {                                                            \
         if (counts) BH_REP_LAUNCH(D, true, true); else BH_REP_LAUNCH(D, false, true); \
@@ -565,17 +631,15 @@ extern "C" int bh_attractive(const int64_t *row_ptr, const int32_t *col,
         return (g == 4 || g == 8 || g == 16 || g == 32) ? g : 16;
     }();
     cudaStream_t st = bh_cs(stream);
+    const AttArgs A{row_ptr, col, val, (const float2 *)y, row_begin, row_end,
+                    exaggeration, sched, (float2 *)attr};
 #define BH_ATTR(G)                                                            \
     {                                                                         \
         const int grid = bh_blocks(row_end - row_begin, 256 / G);             \
         if (padded)                                                           \
-            k_attractive<G, true><<<grid, 256, 0, st>>>(                      \
-                row_ptr, col, val, (const float2 *)y, row_begin, row_end,     \
-                exaggeration, sched, (float2 *)attr);                         \
+            k_attractive<G, true><<<grid, 256, 0, st>>>(A);                   \
         else                                                                  \
-            k_attractive<G, false><<<grid, 256, 0, st>>>(                     \
-                row_ptr, col, val, (const float2 *)y, row_begin, row_end,     \
-                exaggeration, sched, (float2 *)attr);                         \
+            k_attractive<G, false><<<grid, 256, 0, st>>>(A);                  \
     }
     switch (g_env) {
         case 4: BH_ATTR(4) break;
@@ -585,6 +649,70 @@ extern "C" int bh_attractive(const int64_t *row_ptr, const int32_t *col,
     }
 #undef BH_ATTR
     BH_CHECK_LAUNCH("k_attractive");
+    return BH_OK;
+}
+
+extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
+                         double theta, int64_t t_begin, int64_t t_end,
+                         int sorted_out, float *rep, double *zblock,
+                         double *z_out, void *ws, size_t ws_bytes,
+                         const int64_t *row_ptr, const int32_t *col,
+                         const float *val, int64_t n_rows, int padded,
+                         const float *y, int64_t row_begin, int64_t row_end,
+                         float exaggeration, const bh_sched_t *sched,
+                         float *attr, bh_stream_t stream) {
+    BH_REQUIRE(theta >= 0, "theta must be >= 0, got %g", theta);
+    BH_REQUIRE(t_begin >= 0 && t_end <= t->n_points && t_begin <= t_end,
+               "bad point range");
+    BH_REQUIRE(row_begin >= 0 && row_end <= n_rows && row_begin <= row_end,
+               "bad row range");
+    if (t_end == t_begin || row_end == row_begin) {
+        // nothing to overlap: the separate kernels
+        int rc = bh_attractive(row_ptr, col, val, n_rows, padded, y, row_begin,
+                               row_end, exaggeration, sched, attr, stream);
+        if (rc != BH_OK) return rc;
+        return bh_repulsive(t, bounds, theta, nullptr, t_begin, t_end,
+                            sorted_out, rep, nullptr, zblock, z_out, nullptr,
+                            ws, ws_bytes, stream);
+    }
+    BH_REQUIRE(ws_bytes >= bh_repulsive_workspace_bytes(t_end - t_begin),
+               "repulsive workspace too small");
+    // sweeping CTAs per traversal CTA (tuning knob BH_FUSE_RATIO = nr / na)
+    static const int ratio = [] {
+        const char *s = getenv("BH_FUSE_RATIO");
+        const int r = s ? atoi(s) : 2;
+        return r >= 1 ? r : 2;
+    }();
+    constexpr int G = 16;
+    const int64_t nr = rep_grid(t_end - t_begin);
+    const int64_t na = std::max<int64_t>(
+        1, std::min<int64_t>((nr + ratio - 1) / ratio,
+                             bh_blocks(row_end - row_begin, 256 / G)));
+    char *w = (char *)ws;
+    if (!zblock) zblock = (double *)w;
+    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(double) * nr));
+    const RepArgs R{(const float4 *)t->node, (const float2 *)t->ys, t->order,
+                    nullptr, bounds, t->status, theta, t_begin, t_end,
+                    sorted_out, (float2 *)rep, nullptr, nullptr, zblock, ticket,
+                    z_out};
+    const AttArgs A{row_ptr, col, val, (const float2 *)y, row_begin, row_end,
+                    exaggeration, sched, (float2 *)attr};
+    cudaStream_t st = bh_cs(stream);
+    const unsigned grid = (unsigned)(nr + na);
+#define BH_FORCES(D)                                                          \
+    if (padded)                                                               \
+        k_forces<D, G, true><<<grid, kRepThreads, 0, st>>>(R, A, nr, na);     \
+    else                                                                      \
+        k_forces<D, G, false><<<grid, kRepThreads, 0, st>>>(R, A, nr, na);
+    if (t->code_bits == 32) {
+        BH_FORCES(16)
+    } else if (t->code_bits == 64) {
+        BH_FORCES(32)
+    } else {
+        return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
+    }
+#undef BH_FORCES
+    BH_CHECK_LAUNCH("k_forces");
     return BH_OK;
 }
 

@@ -40,7 +40,8 @@ from .quadtree import (DEFAULT_CODE_BITS, TreeArrays, as_points, build_tree,
 
 STAGES = ("knn", "bsp", "tree", "summarize", "attractive", "repulsive",
           "update")
-EXTRA_STAGES = ("comm", "relabel")
+# "forces": the fused attractive + repulsive launch (Engine.fuse_timed)
+EXTRA_STAGES = ("comm", "relabel", "forces")
 MOMENTUM_SWITCH_ITER = 250
 PRECISIONS = ("f32",)
 
@@ -207,9 +208,18 @@ class Engine:
                         "attractive": (7, 3), "repulsive": (3, 4),
                         "update": (5, 6)}
 
+    STAGE_EVENTS_FUSED = {"tree": (0, 1), "summarize": (1, 2),
+                          "forces": (2, 4), "update": (5, 6)}
+
+    def _fused(self, timed: bool) -> bool:
+        return (self.shard is None and self.fuse and not self.overlap
+                and (not timed or self.fuse_timed))
+
     def _stage_events(self):
         if self.shard is not None:
             return self.STAGE_EVENTS_SHARDED
+        if self._fused(True):
+            return self.STAGE_EVENTS_FUSED
         return self.STAGE_EVENTS if self.overlap else self.STAGE_EVENTS_SEQ
 
     def __init__(self, p: SparseAffinity, e: Embedding, cfg: TsneConfig,
@@ -266,6 +276,12 @@ class Engine:
         # (measured +0.6% at C3, profiles/README.md); off by default so the
         # cooperative summarize launch never contends for SM slots
         self.overlap = False
+        # fuse: the untimed fast path launches the fused force pass
+        # (bh_forces); the evented (StepTimings) path keeps the two kernels
+        # apart for the per-stage breakdown unless fuse_timed is set
+        self.fuse = True
+        self.fuse_timed = False
+        self.launches = 0  # library kernels enqueued by run() (bench claim)
         self.fork_ev = torch.cuda.Event()
         self.join_ev = torch.cuda.Event()
         self.shard = shard
@@ -284,12 +300,20 @@ class Engine:
     def val(self):
         return self.csr[self.csr_key][2]
 
-    def kernels_per_iteration(self) -> int:
-        """Kernel launches of one iteration (morton, sort histogram + one
-        pass per byte, 3 tree kernels, one summarize kernel per level,
-        attractive, repulsive, update; + the Z-partials sum when sharded)."""
-        return (1 + 1 + self.code_bits // 8 + 3 + 1
-                + 1 + 1 + 1 + (1 if self.shard is not None else 0))
+    # library kernels of one relabel (invert, 4 row gathers, CSR permute:
+    # 3 scan kernels + last offset + fill) and of one run's load / bounds /
+    # centre / store (3 gathers, 1, 1, 3 scatters)
+    KERNELS_PER_RELABEL = 10
+    KERNELS_PER_RUN = 8
+
+    def kernels_per_iteration(self, timed: bool = False) -> int:
+        """Library kernel launches of one iteration: morton, sort histogram +
+        one pass per code byte, 3 tree kernels, one summarize kernel per
+        level (code_bits / 2 + 1), the force pass (1 fused or attractive +
+        repulsive), update; + the Z-partials sum when sharded."""
+        forces = 1 if self._fused(timed) else 2
+        return (1 + 1 + self.code_bits // 8 + 3 + (self.code_bits // 2 + 1)
+                + forces + 1 + (1 if self.shard is not None else 0))
 
     # -- one iteration -----------------------------------------------------
     def _enqueue(self, ev=None):
@@ -319,7 +343,18 @@ class Engine:
         rec(1)
         t.summarize(st)
         rec(2)
-        if self.shard is None:
+        if self._fused(ev is not None):
+            # both force passes in one launch, their CTAs sharing the SMs
+            # (bitwise the same results as the two kernels)
+            call("bh_forces", t.sref(), ptr(self.bounds), self.theta, 0, n, 0,
+                 ptr(self.rep), None, ptr(self.z_dev), ptr(self.ws_rep),
+                 self.ws_rep.numel(), ptr(self.rp), ptr(self.col),
+                 ptr(self.val), n, 1, ptr(y), 0, n, 1.0, ptr(self.sched),
+                 ptr(self.attr), st)
+            rec(4)
+            rec(5)
+            rep, rep_rank = self.rep, None
+        elif self.shard is None:
             if not self.overlap:  # isolated kernels (stage breakdown)
                 rec(7)
                 call("bh_attractive", ptr(self.rp), ptr(self.col), ptr(self.val),
@@ -345,7 +380,7 @@ class Engine:
                  for _ in range(self.N_EVENTS)] for _ in range(k)]
 
     def _graph(self, k):
-        key = (k, self.csr_key, self.overlap)
+        key = (k, self.csr_key, self.overlap, self._fused(True))
         if key not in self.graphs:
             evs = self._events(k)
             g = torch.cuda.CUDAGraph()
@@ -359,7 +394,7 @@ class Engine:
     def _graph1(self):
         """One iteration without timing events (the fast path: replayed
         back to back, the host only syncs at chunk boundaries)."""
-        key = ("fast", self.csr_key, self.overlap)
+        key = ("fast", self.csr_key, self.overlap, self._fused(False))
         if key not in self.graphs:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.main):
@@ -473,6 +508,7 @@ class Engine:
         caller.wait_stream(self.main)
 
     def _run(self, n_iter, timings, use_graph):
+        self.launches += self.KERNELS_PER_RUN
         self.load()
         self.begin()
         done = 0
@@ -492,6 +528,7 @@ class Engine:
                 for i in range(k):
                     self._enqueue(evs[i] if evs else None)
             done += k
+            self.launches += k * self.kernels_per_iteration(timings is not None)
             self.since_relabel += k
             relabel = (self.relabel_every and done < n_iter
                        and self.since_relabel >= self.relabel_every)
@@ -501,6 +538,7 @@ class Engine:
                 r0.record()
                 self.relabel()
                 r1.record()
+                self.launches += self.KERNELS_PER_RELABEL
             self.main.synchronize()
             self._check()
             if timings is not None:

@@ -316,6 +316,37 @@ def test_engine_graph_equals_eager_and_is_deterministic(bh):
     np.testing.assert_array_equal(outs[0], outs[2])
 
 
+@pytest.mark.parametrize("code_bits", [32, 64])
+def test_fused_forces_bitwise_equal_separate(bh, code_bits):
+    """bh_forces (one launch, interleaved traversal and CSR-sweep CTAs) gives
+    the bitwise trajectory of the separate attractive + repulsive kernels,
+    in the fast path and in the evented path."""
+    rng = np.random.default_rng(5)
+    n, k = 30_000, 24
+    col = rng.integers(0, n - 1, (n, k))
+    col += col >= np.arange(n)[:, None]  # no self edges
+    val = rng.uniform(0.1, 1.0, (n, k)).astype(np.float32)
+    val /= val.sum()
+    p = bh.from_csr(np.arange(0, n * k + 1, k), col.ravel().astype(np.int32),
+                    val.ravel())
+    y0 = rng.standard_normal((n, 2)).astype(np.float32)
+    outs = []
+    for fuse, timed in ((True, False), (False, False), (True, True)):
+        e = bh.embedding_from(y0)
+        cfg = bh.TsneConfig(n_iter=60, exaggeration_iters=20, graph_chunk=10,
+                            code_bits=code_bits, relabel_every=20)
+        eng = bh.Engine(p, e, cfg)
+        eng.fuse = fuse
+        eng.fuse_timed = timed
+        tm = bh.StepTimings() if timed else None
+        eng.run(60, tm)
+        if timed:
+            assert tm.calls("forces") == 60 and tm.calls("repulsive") == 0
+        outs.append(e.y.cpu().numpy().copy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
+
+
 def test_non_finite_gradient_reports_point(bh):
     p = bh.from_csr([0, 1, 2], [1, 0], np.array([0.5, 0.5], np.float32))
     e = bh.embedding_from(np.array([[-1e30, 0.0], [1e30, 0.0]], np.float32))

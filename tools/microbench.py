@@ -80,6 +80,12 @@ def child(args):
     rep = lambda: call("bh_repulsive", t.sref(), ptr(eng.bounds), float(args.theta),
                        None, 0, eng.n, 0, ptr(eng.rep), None, None, ptr(eng.z_dev),
                        None, ptr(eng.ws_rep), eng.ws_rep.numel(), st)
+    fused = lambda: call("bh_forces", t.sref(), ptr(eng.bounds), float(args.theta),
+                         0, eng.n, 0, ptr(eng.rep), None, ptr(eng.z_dev),
+                         ptr(eng.ws_rep), eng.ws_rep.numel(), ptr(eng.rp),
+                         ptr(eng.col), ptr(eng.val), eng.n, 1, ptr(eng.y), 0,
+                         eng.n, 1.0, None, ptr(eng.attr), st)
+
     def sort_build():
         call("bh_sort", ptr(eng.codes), eng.n, 32, ptr(t.sorted_codes),
              ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st)
@@ -89,6 +95,7 @@ def child(args):
            "iteration": args.preroll,
            "attractive_ms": timeit(att, args.reps),
            "repulsive_ms": timeit(rep, args.reps),
+           "forces_fused_ms": timeit(fused, args.reps),
            "sort_build_ms": timeit(sort_build, args.reps),
            "summarize_ms": timeit(lambda: t.summarize(), args.reps)}
     print(json.dumps(out), flush=True)
