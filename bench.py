@@ -290,8 +290,12 @@ def ours_arm(args, rank, world):
     prob = problem(args.config, dev)
     n = int(prob["n"])
     nnz = int(prob["col"].shape[0])
+    if args.precision == "f64":  # the reference's default run precision
+        prob = dict(prob, val=prob["val"].astype(np.float64),
+                    y0=prob["y0"].astype(np.float64))
     p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
-    cfg = bh.TsneConfig(theta=args.theta, graph_chunk=args.chunk)
+    cfg = bh.TsneConfig(theta=args.theta, graph_chunk=args.chunk,
+                        precision=args.precision)
     e = bh.embedding_from(prob["y0"])
     shard = None
     if world > 1:
@@ -356,8 +360,11 @@ def ours_arm(args, rank, world):
     cnt = np.mean(counts, axis=0)
     # 16 B per node record visited (internal + leaf), 8 B per leaf point,
     # 28 B per point (y_i, order, rep out, z) -- SURVEY.md 8(d)
-    rep_bytes = 16.0 * (cnt[0] + cnt[1]) + 8.0 * cnt[2] + 28.0 * n
-    att_bytes = 8.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    # (f64 run precision: 32 B records, 16 B points, 8 B values)
+    w = 2.0 if args.precision == "f64" else 1.0
+    rep_bytes = 16.0 * w * (cnt[0] + cnt[1]) + 8.0 * w * cnt[2] + (
+        28.0 + 16.0 * (w - 1.0)) * n
+    att_bytes = (4.0 + 4.0 * w) * nnz + 4.0 * (n + 1) + 16.0 * w * n
     peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
         peak = float(json.load(open(peaks_path))["hbm_gbs"])
@@ -413,7 +420,7 @@ def ours_arm(args, rank, world):
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (BASELINE.json configs[3] generator, "
+        "dtype": args.precision, "data": "synthetic (BASELINE.json configs[3] generator, "
                                 "SURVEY.md 8(d)); kNN via cuBLAS in setup",
         "config": config_dict(args, n, nnz),
         "e2e": e2e, "gpu_launches": launches,
@@ -622,6 +629,8 @@ def main():
     ap.add_argument("--config", default="c3",
                     choices=["c0", "c1", "c2", "c3", "c4"])
     ap.add_argument("--theta", type=float, default=0.5)
+    ap.add_argument("--precision", choices=["f32", "f64"], default="f32",
+                    help="run precision (f64: the reference's default dtype)")
     ap.add_argument("--chunk", type=int, default=25)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=50)

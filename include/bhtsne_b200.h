@@ -19,8 +19,12 @@
  *    (0) or a negative BH_ERR_* code; `bh_last_error()` (thread-local) then
  *    holds a message.
  *  - Point coordinates are float32 (N, 2) row-major ("(y0, y1)" pairs), the
- *    reference's f32 run mode (io.py:21-30).  Accumulations are float64, as
- *    in the reference kernels.
+ *    reference's f32 run mode (io.py:21-30), with f32 pair arithmetic and
+ *    float64 accumulation.  The `_f64` twins take float64 coordinates
+ *    (and values, forces, velocities, gains) -- the reference's default
+ *    f64 run mode -- and compute every pair term in float64 with the
+ *    reference's operation order.  Trees carry their precision
+ *    (bh_tree_t.precision).
  *  - Morton codes are 32-bit (16 bits per dimension, tree depth <= 16) by
  *    default or 64-bit (the reference's own width, depth <= 32): `code_bits`.
  */
@@ -59,6 +63,7 @@ typedef struct bh_bounds_t {
     float shift0, shift1;
     int32_t nonfinite;
     int32_t code_bits;
+    double shift0_f64, shift1_f64; /* the pending re-centering, f64 mode */
 } bh_bounds_t;
 
 /* Optimiser schedule, resident on the device so that whole iterations can be
@@ -79,6 +84,10 @@ typedef struct bh_sched_t {
     float pad1;
     int64_t bad;
     double z;
+    /* the same schedule constants as float64 (the f64 run mode) */
+    double exaggeration_f64;
+    double momentum_early_f64, momentum_late_f64;
+    double learning_rate_f64, min_gain_f64;
 } bh_sched_t;
 
 /* Node record of the level-contiguous quadtree (16 bytes):
@@ -88,6 +97,8 @@ typedef struct bh_sched_t {
  *           internal -> bits 0..28 = first child node, bits 29..30 =
  *           (number of children - 1).  Children of a node are consecutive
  *           in the next level, in Morton-digit order (quadtree.py:66-85). */
+/* f64 trees (precision 64) use 32-byte records: {x, y} as float64, then
+ * {mass, info, 0, 0} as uint32 -- two 16-byte words. */
 #define BH_LEAF_BIT 0x80000000u
 #define BH_CHILD_MASK 0x1FFFFFFFu
 #define BH_NKIDS_SHIFT 29
@@ -100,7 +111,7 @@ typedef struct bh_tree_t {
     int64_t node_capacity;
     int32_t code_bits; /* 32 or 64 */
     int32_t max_depth; /* code_bits / 2 */
-    float *node;       /* 4 * node_capacity floats: records as above */
+    float *node;       /* node_capacity records as above (16 or 32 B) */
     int32_t *parent;   /* node_capacity: parent node, -1 for the root */
     int32_t *node_start; /* node_capacity: first point (sorted order) */
     int32_t *leaf_end;   /* node_capacity: one past the last point (leaves) */
@@ -108,9 +119,12 @@ typedef struct bh_tree_t {
                             off[max_depth + 2] = number of levels */
     int32_t *order;      /* n: sorted position -> point id */
     void *sorted_codes;  /* n codes (uint32 or uint64) */
-    float *ys;           /* 2n: coordinates in sorted order (quadtree.py:476) */
+    float *ys;           /* 2n: coordinates in sorted order (quadtree.py:476),
+                            float32 or float64 per `precision` */
     int32_t *status;     /* device int32: BH_OK or BH_ERR_CAPACITY after build */
     int32_t *rank;       /* optional n: rank[order[t]] = t (NULL: skipped) */
+    int32_t precision;   /* 32 (default, also 0) or 64: y/ys/record type */
+    int32_t pad;
 } bh_tree_t;
 
 const char *bh_last_error(void);
@@ -126,6 +140,11 @@ int bh_bounds(const float *y, int64_t n, int code_bits, bh_bounds_t *out,
  * (shift0, shift1) (the fused update/centering of gradient_step). */
 int bh_morton(float *y, int64_t n, const bh_bounds_t *bounds, int code_bits,
               int apply_shift, void *codes, bh_stream_t stream);
+int bh_bounds_f64(const double *y, int64_t n, int code_bits, bh_bounds_t *out,
+                  void *ws, size_t ws_bytes, bh_stream_t stream);
+int bh_morton_f64(double *y, int64_t n, const bh_bounds_t *bounds,
+                  int code_bits, int apply_shift, void *codes,
+                  bh_stream_t stream);
 
 /* ---- stable radix sort: _radix_argsort (quadtree.py:188-227) ------------
  * Sorts keys (uint32 when key_bits <= 32, else uint64) with ids 0..n-1 as
@@ -145,12 +164,13 @@ int bh_sort_pairs(const void *keys, const uint32_t *vals, int64_t n,
  * ys = y[order].  On overflow of node_capacity, *tree->status is set to
  * BH_ERR_CAPACITY and the tree is left incomplete. */
 size_t bh_tree_workspace_bytes(int64_t n, int code_bits);
-int bh_build_tree(const bh_tree_t *tree, const float *y, void *ws,
+int bh_build_tree(const bh_tree_t *tree, const void *y, void *ws,
                   size_t ws_bytes, bh_stream_t stream);
+/* y: float32 or float64 (N, 2) per tree->precision. */
 
 /* ---- summarize (quadtree.py:481-519) --------------------------------------
  * Bottom-up centre of mass and count; bit-identical to the reference
- * (f64 sums in reference order, stored as float32). */
+ * (f64 sums in reference order, stored in the tree's precision). */
 int bh_summarize(const bh_tree_t *tree, void *ws, size_t ws_bytes,
                  bh_stream_t stream);
 /* ws: the bh_tree_workspace_bytes() workspace (holds a grid barrier; all
@@ -199,6 +219,19 @@ int bh_forces(const bh_tree_t *tree, const bh_bounds_t *bounds, double theta,
               int64_t n_rows, int padded, const float *y, int64_t row_begin,
               int64_t row_end, float exaggeration, const bh_sched_t *sched,
               float *attr, bh_stream_t stream);
+/* f64 twins (tree->precision 64): float64 values, coordinates and forces;
+ * pair terms in float64 in the reference's operation order, acceptance
+ * (2r)^2 < theta^2 d^2 evaluated in float64 as forces.py:112-116. */
+int bh_attractive_f64(const int64_t *row_ptr, const int32_t *col,
+                      const double *val, int64_t n_rows, int padded,
+                      const double *y, int64_t row_begin, int64_t row_end,
+                      double exaggeration, const bh_sched_t *sched,
+                      double *attr, bh_stream_t stream);
+int bh_repulsive_f64(const bh_tree_t *tree, const bh_bounds_t *bounds,
+                     double theta, const double *y_query, int64_t t_begin,
+                     int64_t t_end, int sorted_out, double *rep, double *zpart,
+                     double *zblock, double *z_out, int32_t *counts, void *ws,
+                     size_t ws_bytes, bh_stream_t stream);
 /* *out = fixed-order sum of n per-CTA Z partials (see bh_repulsive). */
 int bh_sum_partials(const double *x, int64_t n, double *out,
                     bh_stream_t stream);
@@ -209,6 +242,9 @@ size_t bh_repulsive_exact_workspace_bytes(int64_t n);
 int bh_repulsive_exact(const float *y, int64_t n, float *rep, double *zpart,
                        double *z_out, void *ws, size_t ws_bytes,
                        bh_stream_t stream);
+int bh_repulsive_exact_f64(const double *y, int64_t n, double *rep,
+                           double *zpart, double *z_out, void *ws,
+                           size_t ws_bytes, bh_stream_t stream);
 
 /* ---- KL divergence rows (optimizer.py:227-239) ---------------------------
  * *kl_out = sum_i sum_t p ln(p Z (1+d^2)) with Z read from *z (device). */
@@ -216,6 +252,10 @@ size_t bh_kl_workspace_bytes(int64_t n);
 int bh_kl_rows(const int64_t *row_ptr, const int32_t *col, const float *val,
                int64_t n, int padded, const float *y, const double *z,
                double *kl_out, void *ws, size_t ws_bytes, bh_stream_t stream);
+int bh_kl_rows_f64(const int64_t *row_ptr, const int32_t *col,
+                   const double *val, int64_t n, int padded, const double *y,
+                   const double *z, double *kl_out, void *ws, size_t ws_bytes,
+                   bh_stream_t stream);
 
 /* ---- momentum / gains update (optimizer.py:161-168, 195-224) -------------
  * grad = 4 (attr - rep / f32(Z)); gains, velocity, y += v, then the mean of
@@ -233,12 +273,24 @@ int bh_update(float *y, float *v, float *g, const float *attr,
               bh_stream_t stream);
 int bh_center(float *y, int64_t n, const bh_bounds_t *bounds,
               bh_stream_t stream);
+/* f64 run mode: grad = 4 (attr - rep / Z) with Z in float64, the update in
+ * float64 (optimizer.py:161-168 on float64 arrays), shift*_f64 = the f64
+ * mean; schedule constants from the *_f64 fields of sched. */
+int bh_update_f64(double *y, double *v, double *g, const double *attr,
+                  const double *rep, const int32_t *rep_rank, int64_t n,
+                  bh_sched_t *sched, bh_bounds_t *bounds_out, int code_bits,
+                  void *ws, size_t ws_bytes, bh_stream_t stream);
+int bh_center_f64(double *y, int64_t n, const bh_bounds_t *bounds,
+                  bh_stream_t stream);
 
 /* ---- binary-search perplexity: calibrate_perplexity (affinity.py:61-118) --
  * One warp per row, f64 bisection with the reference's exact schedule. */
 int bh_bsp(const float *sqd, int64_t n, int64_t k, double perplexity,
            double tol_bits, int64_t max_iter, double *betas, double *cond,
            bh_stream_t stream);
+int bh_bsp_f64(const double *sqd, int64_t n, int64_t k, double perplexity,
+               double tol_bits, int64_t max_iter, double *betas, double *cond,
+               bh_stream_t stream);
 
 /* ---- symmetrize (affinity.py:121-158) ------------------------------------
  * p_ij = max((p_j|i + p_i|j) / 2N, eps64) as float32 CSR with ascending
@@ -254,6 +306,11 @@ int bh_symmetrize_fill(const double *cond, int64_t n, int64_t k,
                        const int64_t *nnz, int64_t *row_ptr, int32_t *col,
                        float *val, void *ws, size_t ws_bytes,
                        bh_stream_t stream);
+/* f64 run mode: values stay float64 (no final cast). */
+int bh_symmetrize_fill_f64(const double *cond, int64_t n, int64_t k,
+                           const int64_t *nnz, int64_t *row_ptr, int32_t *col,
+                           double *val, void *ws, size_t ws_bytes,
+                           bh_stream_t stream);
 /* Pads a CSR so every row starts at a multiple of 4 entries (pad entries:
  * col = row, val = 0).  out_row_ptr has n+1 entries; out capacity from
  * bh_pad_csr_size (device int64 result in *padded_nnz). */
@@ -264,11 +321,16 @@ int bh_pad_csr_size(const int64_t *row_ptr, int64_t n, int64_t *out_row_ptr,
 int bh_pad_csr_fill(const int64_t *row_ptr, const int32_t *col,
                     const float *val, int64_t n, const int64_t *out_row_ptr,
                     int32_t *out_col, float *out_val, bh_stream_t stream);
+int bh_pad_csr_fill_f64(const int64_t *row_ptr, const int32_t *col,
+                        const double *val, int64_t n,
+                        const int64_t *out_row_ptr, int32_t *out_col,
+                        double *out_val, bh_stream_t stream);
 
 /* ---- relabeling (engine-internal locality; not a reference interface) ----
  * The optimiser periodically renumbers points in the current Morton order so
  * that CSR rows, their column gathers and the traversal's outputs are
- * spatially coherent.  perm[new] = old, rank[old] = new. */
+ * spatially coherent.  perm[new] = old, rank[old] = new.  Row gathers and
+ * scatters move elem_bytes = 4, 8 or 16 bytes per row. */
 int bh_gather_rows(const void *src, const int32_t *idx, int64_t n,
                    int elem_bytes, void *dst, bh_stream_t stream);
 int bh_scatter_rows(const void *src, const int32_t *idx, int64_t n,
@@ -280,6 +342,11 @@ int bh_permute_csr(const int64_t *row_ptr, const int32_t *col, const float *val,
                    const int32_t *perm, const int32_t *rank, int64_t n,
                    int64_t *out_row_ptr, int32_t *out_col, float *out_val,
                    void *ws, size_t ws_bytes, bh_stream_t stream);
+int bh_permute_csr_f64(const int64_t *row_ptr, const int32_t *col,
+                       const double *val, const int32_t *perm,
+                       const int32_t *rank, int64_t n, int64_t *out_row_ptr,
+                       int32_t *out_col, double *out_val, void *ws,
+                       size_t ws_bytes, bh_stream_t stream);
 
 /* ---- exact kNN (knn.py:36-73) ---------------------
  * f64 squared distances summed over columns in order, k smallest per row,
@@ -287,6 +354,9 @@ int bh_permute_csr(const int64_t *row_ptr, const int32_t *col, const float *val,
  * x: (n, d) float32 row-major, d <= 64, k <= 128. */
 int bh_knn(const float *x, int64_t n, int64_t d, int64_t k, int64_t *out_idx,
            float *out_sqd, bh_stream_t stream);
+/* f64 run mode: float64 data, distances returned as float64. */
+int bh_knn_f64(const double *x, int64_t n, int64_t d, int64_t k,
+               int64_t *out_idx, double *out_sqd, bh_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -28,14 +28,17 @@ BH_ERR_CAPACITY = -3
 BOUNDS_DTYPE = np.dtype([
     ("c0", "f8"), ("c1", "f8"), ("r_span", "f8"), ("root0", "f8"),
     ("root1", "f8"), ("scale", "f8"), ("shift0", "f4"), ("shift1", "f4"),
-    ("nonfinite", "i4"), ("code_bits", "i4")])
+    ("nonfinite", "i4"), ("code_bits", "i4"), ("shift0_f64", "f8"),
+    ("shift1_f64", "f8")])
 SCHED_DTYPE = np.dtype([
     ("iteration", "i4"), ("exaggeration_iters", "i4"),
     ("momentum_switch", "i4"), ("pad0", "i4"), ("exaggeration", "f4"),
     ("momentum_early", "f4"), ("momentum_late", "f4"),
     ("learning_rate", "f4"), ("min_gain", "f4"), ("pad1", "f4"),
-    ("bad", "i8"), ("z", "f8")])
-assert BOUNDS_DTYPE.itemsize == 64 and SCHED_DTYPE.itemsize == 56
+    ("bad", "i8"), ("z", "f8"), ("exaggeration_f64", "f8"),
+    ("momentum_early_f64", "f8"), ("momentum_late_f64", "f8"),
+    ("learning_rate_f64", "f8"), ("min_gain_f64", "f8")])
+assert BOUNDS_DTYPE.itemsize == 80 and SCHED_DTYPE.itemsize == 96
 INT64_MAX = np.iinfo(np.int64).max
 
 
@@ -51,6 +54,7 @@ class TreeStruct(C.Structure):
         ("sorted_codes", C.c_void_p), ("ys", C.c_void_p),
         ("status", C.c_void_p),
         ("rank", C.c_void_p),
+        ("precision", C.c_int32), ("pad", C.c_int32),
     ]
 
 
@@ -80,6 +84,27 @@ SIGNATURES = {
                    _P, _P, _P, _P, _SZ, _P, _P, _P, _I64, C.c_int, _P, _I64,
                    _I64, C.c_float, _P, _P, _P], C.c_int),
     "bh_sum_partials": ([_P, _I64, _P, _P], C.c_int),
+    "bh_attractive_f64": ([_P, _P, _P, _I64, C.c_int, _P, _I64, _I64,
+                           C.c_double, _P, _P, _P], C.c_int),
+    "bh_repulsive_f64": ([C.POINTER(TreeStruct), _P, C.c_double, _P, _I64,
+                          _I64, C.c_int, _P, _P, _P, _P, _P, _P, _SZ, _P],
+                         C.c_int),
+    "bh_repulsive_exact_f64": ([_P, _I64, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_kl_rows_f64": ([_P, _P, _P, _I64, C.c_int, _P, _P, _P, _P, _SZ, _P],
+                       C.c_int),
+    "bh_bounds_f64": ([_P, _I64, C.c_int, _P, _P, _SZ, _P], C.c_int),
+    "bh_morton_f64": ([_P, _I64, _P, C.c_int, C.c_int, _P, _P], C.c_int),
+    "bh_update_f64": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P, C.c_int, _P,
+                       _SZ, _P], C.c_int),
+    "bh_center_f64": ([_P, _I64, _P, _P], C.c_int),
+    "bh_bsp_f64": ([_P, _I64, _I64, C.c_double, C.c_double, _I64, _P, _P,
+                    _P], C.c_int),
+    "bh_symmetrize_fill_f64": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P],
+                               C.c_int),
+    "bh_pad_csr_fill_f64": ([_P, _P, _P, _I64, _P, _P, _P, _P], C.c_int),
+    "bh_permute_csr_f64": ([_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _SZ,
+                            _P], C.c_int),
+    "bh_knn_f64": ([_P, _I64, _I64, _I64, _P, _P, _P], C.c_int),
     "bh_repulsive_exact_workspace_bytes": ([_I64], _SZ),
     "bh_repulsive_exact": ([_P, _I64, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "bh_kl_workspace_bytes": ([_I64], _SZ),
@@ -148,6 +173,39 @@ def check(rc: int, what: str = "") -> None:
 def call(name: str, *args):
     lib = load()
     check(getattr(lib, name)(*args), name)
+
+
+# Run precision: the reference's dtype (io.py:21-30).  f64 tensors select the
+# library's `_f64` entry points.
+DTYPES = {"f32": torch.float32, "f64": torch.float64}
+
+
+def is_f64(t) -> bool:
+    dt = t.dtype if isinstance(t, torch.Tensor) else t
+    return dt in (torch.float64, np.float64, np.dtype(np.float64))
+
+
+def fn(name: str, dtype) -> str:
+    """Entry point for a run precision: bh_x or bh_x_f64."""
+    return name + "_f64" if is_f64(dtype) else name
+
+
+def torch_dtype(dtype) -> torch.dtype:
+    """numpy/torch/str precision -> torch.float32 | torch.float64."""
+    if isinstance(dtype, str):
+        if dtype not in DTYPES:
+            raise ValueError(f"unknown precision {dtype!r}; expected one of "
+                             f"{sorted(DTYPES)}")
+        return DTYPES[dtype]
+    if isinstance(dtype, torch.dtype):
+        dt = dtype
+    else:
+        dt = {np.dtype(np.float32): torch.float32,
+              np.dtype(np.float64): torch.float64}.get(np.dtype(dtype))
+    if dt not in (torch.float32, torch.float64):
+        raise ValueError(f"unsupported dtype {dtype}; expected float32 or "
+                         "float64")
+    return dt
 
 
 def ptr(t: torch.Tensor | None):

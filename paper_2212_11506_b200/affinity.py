@@ -6,9 +6,10 @@ pkg/src/bhtsne/affinity.py, knn.py:20-33): ``NeighborGraph``,
 (:99-118), ``symmetrize`` (:121-158), ``set_exaggeration`` (:161-173).
 
 Device layout: CSR with int64 ``row_offsets``, int32 ``col_indices`` and
-float32 ``base_values`` (the pristine, unexaggerated p_ij).  The
-exaggeration factor is applied inside the kernels as ``base * f32(factor)``
--- the same float32 product set_exaggeration computes -- so rescaling never
+``base_values`` (the pristine, unexaggerated p_ij) in the run precision,
+float32 or float64 (symmetrize's ``dtype``, affinity.py:121-158).  The
+exaggeration factor is applied inside the kernels as ``base * dtype(factor)``
+-- the same product set_exaggeration computes -- so rescaling never
 rewrites the matrix and restoring factor 1 is bitwise exact.
 """
 
@@ -33,7 +34,7 @@ class NeighborGraph:
     (knn.py:20-33).  Accepts numpy or torch; stored on the device."""
 
     indices: torch.Tensor       # (N, k) int64
-    sq_distances: torch.Tensor  # (N, k) float32
+    sq_distances: torch.Tensor  # (N, k) float32 or float64 (the data's dtype)
 
     def __post_init__(self):
         dev = _lib.device()
@@ -45,8 +46,9 @@ class NeighborGraph:
             raise ValueError("indices and sq_distances must be (N, k)")
         object.__setattr__(self, "indices",
                            idx.to(dev, torch.int64).contiguous())
+        sdt = torch.float64 if sqd.dtype == torch.float64 else torch.float32
         object.__setattr__(self, "sq_distances",
-                           sqd.to(dev, torch.float32).contiguous())
+                           sqd.to(dev, sdt).contiguous())
 
     @property
     def n_points(self) -> int:
@@ -70,7 +72,7 @@ class SparseAffinity:
     n: int
     row_offsets: torch.Tensor  # (N+1,) int64
     col_indices: torch.Tensor  # (nnz,) int32
-    base_values: torch.Tensor  # (nnz,) float32, exaggeration 1
+    base_values: torch.Tensor  # (nnz,) float32 | float64, exaggeration 1
     exaggeration: float = 1.0
     _padded: dict = field(default_factory=dict, repr=False, compare=False)
 
@@ -80,11 +82,16 @@ class SparseAffinity:
 
     @property
     def values(self) -> torch.Tensor:
-        """Currently applied values (base * f32(factor), affinity.py:171)."""
+        """Currently applied values (base * dtype(factor), affinity.py:171)."""
         if self.exaggeration == 1.0:
             return self.base_values
         return self.base_values * torch.tensor(
-            np.float32(self.exaggeration), device=self.base_values.device)
+            self.exaggeration, dtype=self.base_values.dtype,
+            device=self.base_values.device)
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.base_values.dtype
 
     def padded(self):
         """(row_ptr, col, val) with rows padded to multiples of 4 entries
@@ -126,16 +133,15 @@ def calibrate_perplexity(g, u: float, max_iter: int = DEFAULT_MAX_ITER,
     dev = g.indices.device
     cond = torch.empty((n, k), dtype=torch.float64, device=dev)
     betas = torch.empty(n, dtype=torch.float64, device=dev)
-    call("bh_bsp", ptr(g.sq_distances), n, k, float(u), float(tol),
-         int(max_iter), ptr(betas), ptr(cond), stream())
+    call(_lib.fn("bh_bsp", g.sq_distances.dtype), ptr(g.sq_distances), n, k,
+         float(u), float(tol), int(max_iter), ptr(betas), ptr(cond), stream())
     return PerplexityResult(betas=betas, conditional=cond)
 
 
 def symmetrize(pr: PerplexityResult, g, dtype=np.float32) -> SparseAffinity:
-    """p_ij = max((p_j|i + p_i|j) / 2N, eps64) as float32 CSR."""
+    """p_ij = max((p_j|i + p_i|j) / 2N, eps64) as a ``dtype`` CSR."""
     g = as_graph(g)
-    if np.dtype(dtype) != np.float32:
-        raise ValueError("the B200 path stores P in float32 (precision 'f32')")
+    dt = _lib.torch_dtype(dtype)
     n, k = g.indices.shape
     if tuple(pr.conditional.shape) != (n, k):
         raise ValueError("perplexity result does not match neighbor graph")
@@ -148,16 +154,18 @@ def symmetrize(pr: PerplexityResult, g, dtype=np.float32) -> SparseAffinity:
     nnz = int(nnz_t.item())
     row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
     col = torch.empty(nnz, dtype=torch.int32, device=dev)
-    val = torch.empty(nnz, dtype=torch.float32, device=dev)
-    call("bh_symmetrize_fill", ptr(pr.conditional), n, k, ptr(nnz_t),
-         ptr(row_ptr), ptr(col), ptr(val), ptr(ws), ws.numel(), stream())
+    val = torch.empty(nnz, dtype=dt, device=dev)
+    call(_lib.fn("bh_symmetrize_fill", dt), ptr(pr.conditional), n, k,
+         ptr(nnz_t), ptr(row_ptr), ptr(col), ptr(val), ptr(ws), ws.numel(),
+         stream())
     del ws
     return SparseAffinity(n=n, row_offsets=row_ptr, col_indices=col,
                           base_values=val, exaggeration=1.0)
 
 
 def from_csr(row_offsets, col_indices, values, n=None) -> SparseAffinity:
-    """Wrap a host/device CSR (e.g. the reference's SparseAffinity arrays)."""
+    """Wrap a host/device CSR (e.g. the reference's SparseAffinity arrays);
+    float64 values stay float64 (the f64 run mode), others become float32."""
     dev = _lib.device()
     ro = torch.as_tensor(np.asarray(row_offsets, np.int64)
                          if not isinstance(row_offsets, torch.Tensor)
@@ -165,9 +173,10 @@ def from_csr(row_offsets, col_indices, values, n=None) -> SparseAffinity:
     ci = torch.as_tensor(np.asarray(col_indices)
                          if not isinstance(col_indices, torch.Tensor)
                          else col_indices).to(dev, torch.int32).contiguous()
-    va = torch.as_tensor(np.asarray(values, np.float32)
-                         if not isinstance(values, torch.Tensor)
-                         else values).to(dev, torch.float32).contiguous()
+    va = torch.as_tensor(np.asarray(values)
+                         if not isinstance(values, torch.Tensor) else values)
+    vdt = torch.float64 if va.dtype == torch.float64 else torch.float32
+    va = va.to(dev, vdt).contiguous()
     return SparseAffinity(n=int(n if n is not None else ro.shape[0] - 1),
                           row_offsets=ro, col_indices=ci, base_values=va)
 
@@ -194,7 +203,7 @@ def pad_csr(row_ptr, col, val):
          ws.numel(), stream())
     m = int(total.item())
     ocol = torch.empty(m, dtype=torch.int32, device=dev)
-    oval = torch.empty(m, dtype=torch.float32, device=dev)
-    call("bh_pad_csr_fill", ptr(row_ptr), ptr(col), ptr(val), n, ptr(out_rp),
-         ptr(ocol), ptr(oval), stream())
+    oval = torch.empty(m, dtype=val.dtype, device=dev)
+    call(_lib.fn("bh_pad_csr_fill", val.dtype), ptr(row_ptr), ptr(col),
+         ptr(val), n, ptr(out_rp), ptr(ocol), ptr(oval), stream())
     return out_rp, ocol, oval

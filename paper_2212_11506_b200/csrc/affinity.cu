@@ -15,16 +15,16 @@ namespace bh {
 // lane-strided partials + a butterfly, so all lanes agree bit for bit and
 // take identical branches.
 // ---------------------------------------------------------------------------
-template <int KPL>
+template <int KPL, typename S>
 __global__ void __launch_bounds__(256)
-k_bsp(const float *__restrict__ sqd, int64_t n, int k, double ln_u,
+k_bsp(const S *__restrict__ sqd, int64_t n, int k, double ln_u,
       double tol, int max_iter, double *__restrict__ betas,
       double *__restrict__ cond) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t row = wid; row < n; row += nw) {
-        const float *r = sqd + row * (int64_t)k;
+        const S *r = sqd + row * (int64_t)k;
         double *out = cond + row * (int64_t)k;
         const double dmax = (double)r[k - 1];
         if (dmax <= 0.0) {
@@ -177,12 +177,13 @@ struct UniqueFlag {
     }
 };
 
+template <typename V>
 __global__ void k_sym_fill(const uint64_t *__restrict__ keys,
                            const uint32_t *__restrict__ vals,
                            const uint32_t *__restrict__ pos, int64_t m,
                            const double *__restrict__ cond, int64_t n,
                            int64_t *__restrict__ row_ptr,
-                           int32_t *__restrict__ col, float *__restrict__ val,
+                           int32_t *__restrict__ col, V *__restrict__ val,
                            const int64_t *__restrict__ nnz) {
     const double two_n = 2.0 * (double)n;
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < m;
@@ -196,7 +197,7 @@ __global__ void k_sym_fill(const uint64_t *__restrict__ keys,
         if (p < DBL_EPSILON) p = DBL_EPSILON;
         const int64_t row = (int64_t)(key / (uint64_t)n);
         col[o] = (int32_t)(key % (uint64_t)n);
-        val[o] = __double2float_rn(p);
+        val[o] = (V)p;  // .astype(dtype): round to nearest for f32
         // first entry of its row: fill row_ptr for this row and any empty
         // rows before it; the last entry also closes the trailing rows
         const int64_t prev = (o == 0) ? -1 : (int64_t)(keys[u - 1] / (uint64_t)n);
@@ -247,11 +248,12 @@ __global__ void k_pad_finish(const int64_t *__restrict__ rp, int64_t n,
     if (blockIdx.x == 0 && threadIdx.x == 0) out_rp[n] = *total;
 }
 
+template <typename V>
 __global__ void k_pad_fill(const int64_t *__restrict__ rp,
                            const int32_t *__restrict__ col,
-                           const float *__restrict__ val, int64_t n,
+                           const V *__restrict__ val, int64_t n,
                            const int64_t *__restrict__ orp,
-                           int32_t *__restrict__ ocol, float *__restrict__ oval) {
+                           int32_t *__restrict__ ocol, V *__restrict__ oval) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -260,7 +262,7 @@ __global__ void k_pad_fill(const int64_t *__restrict__ rp,
         const int64_t plen = orp[r + 1] - o;
         for (int64_t q = lane; q < plen; q += 32) {
             ocol[o + q] = q < len ? col[s + q] : (int32_t)r;
-            oval[o + q] = q < len ? val[s + q] : 0.0f;
+            oval[o + q] = q < len ? val[s + q] : V(0);
         }
     }
 }
@@ -269,9 +271,10 @@ __global__ void k_pad_fill(const int64_t *__restrict__ rp,
 
 using namespace bh;
 
-extern "C" int bh_bsp(const float *sqd, int64_t n, int64_t k,
-                      double perplexity, double tol_bits, int64_t max_iter,
-                      double *betas, double *cond, bh_stream_t stream) {
+template <typename S>
+static int bsp_impl(const S *sqd, int64_t n, int64_t k, double perplexity,
+                    double tol_bits, int64_t max_iter, double *betas,
+                    double *cond, bh_stream_t stream) {
     BH_REQUIRE(k >= 1 && k <= 1024, "k must be in [1, 1024] for bh_bsp");
     BH_REQUIRE(perplexity <= (double)k,
                "perplexity exceeds neighborhood size (u=%g, k=%lld)", perplexity,
@@ -285,7 +288,7 @@ extern "C" int bh_bsp(const float *sqd, int64_t n, int64_t k,
     cudaStream_t st = bh_cs(stream);
     const int kpl = (int)((k + 31) / 32);
 #define BH_BSP(KPL)                                                           \
-    k_bsp<KPL><<<grid, 256, 0, st>>>(sqd, n, (int)k, ln_u, tol, (int)max_iter, \
+    k_bsp<KPL, S><<<grid, 256, 0, st>>>(sqd, n, (int)k, ln_u, tol, (int)max_iter, \
                                      betas, cond)
     if (kpl <= 1) BH_BSP(1);
     else if (kpl <= 2) BH_BSP(2);
@@ -297,6 +300,20 @@ extern "C" int bh_bsp(const float *sqd, int64_t n, int64_t k,
 #undef BH_BSP
     BH_CHECK_LAUNCH("k_bsp");
     return BH_OK;
+}
+
+extern "C" int bh_bsp(const float *sqd, int64_t n, int64_t k,
+                      double perplexity, double tol_bits, int64_t max_iter,
+                      double *betas, double *cond, bh_stream_t stream) {
+    return bsp_impl(sqd, n, k, perplexity, tol_bits, max_iter, betas, cond,
+                    stream);
+}
+
+extern "C" int bh_bsp_f64(const double *sqd, int64_t n, int64_t k,
+                          double perplexity, double tol_bits, int64_t max_iter,
+                          double *betas, double *cond, bh_stream_t stream) {
+    return bsp_impl(sqd, n, k, perplexity, tol_bits, max_iter, betas, cond,
+                    stream);
 }
 
 extern "C" size_t bh_symmetrize_workspace_bytes(int64_t n, int64_t k) {
@@ -332,20 +349,36 @@ extern "C" int bh_symmetrize_plan(const int64_t *indices, int64_t n, int64_t k,
     return cuda_status(e, "symmetrize nnz");
 }
 
-extern "C" int bh_symmetrize_fill(const double *cond, int64_t n, int64_t k,
-                                  const int64_t *nnz, int64_t *row_ptr,
-                                  int32_t *col, float *val, void *ws,
-                                  size_t ws_bytes, bh_stream_t stream) {
+template <typename V>
+static int sym_fill_impl(const double *cond, int64_t n, int64_t k,
+                         const int64_t *nnz, int64_t *row_ptr, int32_t *col,
+                         V *val, void *ws, size_t ws_bytes, bh_stream_t stream) {
     SymLayout L = sym_layout(n, k);
     BH_REQUIRE(ws_bytes >= L.total, "symmetrize workspace too small");
     char *w = (char *)ws;
     int grid = bh_blocks(L.m, 256);
     if (grid > kSMs * 32) grid = kSMs * 32;
-    k_sym_fill<<<grid, 256, 0, bh_cs(stream)>>>(
+    k_sym_fill<V><<<grid, 256, 0, bh_cs(stream)>>>(
         (const uint64_t *)(w + L.skeys), (const uint32_t *)(w + L.svals),
         (const uint32_t *)(w + L.pos), L.m, cond, n, row_ptr, col, val, nnz);
     BH_CHECK_LAUNCH("k_sym_fill");
     return BH_OK;
+}
+
+extern "C" int bh_symmetrize_fill(const double *cond, int64_t n, int64_t k,
+                                  const int64_t *nnz, int64_t *row_ptr,
+                                  int32_t *col, float *val, void *ws,
+                                  size_t ws_bytes, bh_stream_t stream) {
+    return sym_fill_impl(cond, n, k, nnz, row_ptr, col, val, ws, ws_bytes,
+                         stream);
+}
+
+extern "C" int bh_symmetrize_fill_f64(const double *cond, int64_t n, int64_t k,
+                                      const int64_t *nnz, int64_t *row_ptr,
+                                      int32_t *col, double *val, void *ws,
+                                      size_t ws_bytes, bh_stream_t stream) {
+    return sym_fill_impl(cond, n, k, nnz, row_ptr, col, val, ws, ws_bytes,
+                         stream);
 }
 
 extern "C" size_t bh_pad_csr_workspace_bytes(int64_t n) {
@@ -364,16 +397,32 @@ extern "C" int bh_pad_csr_size(const int64_t *row_ptr, int64_t n,
     return BH_OK;
 }
 
+template <typename V>
+static int pad_fill_impl(const int64_t *row_ptr, const int32_t *col,
+                         const V *val, int64_t n, const int64_t *out_row_ptr,
+                         int32_t *out_col, V *out_val, bh_stream_t stream) {
+    int grid = bh_blocks(n, 8);
+    if (grid > kSMs * 32) grid = kSMs * 32;
+    k_pad_fill<V><<<grid, 256, 0, bh_cs(stream)>>>(row_ptr, col, val, n,
+                                                   out_row_ptr, out_col, out_val);
+    BH_CHECK_LAUNCH("k_pad_fill");
+    return BH_OK;
+}
+
 extern "C" int bh_pad_csr_fill(const int64_t *row_ptr, const int32_t *col,
                                const float *val, int64_t n,
                                const int64_t *out_row_ptr, int32_t *out_col,
                                float *out_val, bh_stream_t stream) {
-    int grid = bh_blocks(n, 8);
-    if (grid > kSMs * 32) grid = kSMs * 32;
-    k_pad_fill<<<grid, 256, 0, bh_cs(stream)>>>(row_ptr, col, val, n, out_row_ptr,
-                                                out_col, out_val);
-    BH_CHECK_LAUNCH("k_pad_fill");
-    return BH_OK;
+    return pad_fill_impl(row_ptr, col, val, n, out_row_ptr, out_col, out_val,
+                         stream);
+}
+
+extern "C" int bh_pad_csr_fill_f64(const int64_t *row_ptr, const int32_t *col,
+                                   const double *val, int64_t n,
+                                   const int64_t *out_row_ptr, int32_t *out_col,
+                                   double *out_val, bh_stream_t stream) {
+    return pad_fill_impl(row_ptr, col, val, n, out_row_ptr, out_col, out_val,
+                         stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -392,14 +441,15 @@ struct PermLen {
     }
 };
 
+template <typename V>
 __global__ void k_permute_csr_fill(const int64_t *__restrict__ rp,
                                    const int32_t *__restrict__ col,
-                                   const float *__restrict__ val,
+                                   const V *__restrict__ val,
                                    const int32_t *__restrict__ perm,
                                    const int32_t *__restrict__ rank, int64_t n,
                                    const int64_t *__restrict__ orp,
                                    int32_t *__restrict__ ocol,
-                                   float *__restrict__ oval) {
+                                   V *__restrict__ oval) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -423,12 +473,12 @@ extern "C" size_t bh_permute_csr_workspace_bytes(int64_t n) {
     return scan_ws<int64_t, PermLen>(n) + 256;
 }
 
-extern "C" int bh_permute_csr(const int64_t *row_ptr, const int32_t *col,
-                              const float *val, const int32_t *perm,
-                              const int32_t *rank, int64_t n,
-                              int64_t *out_row_ptr, int32_t *out_col,
-                              float *out_val, void *ws, size_t ws_bytes,
-                              bh_stream_t stream) {
+template <typename V>
+static int permute_impl(const int64_t *row_ptr, const int32_t *col,
+                        const V *val, const int32_t *perm, const int32_t *rank,
+                        int64_t n, int64_t *out_row_ptr, int32_t *out_col,
+                        V *out_val, void *ws, size_t ws_bytes,
+                        bh_stream_t stream) {
     BH_REQUIRE(ws_bytes >= bh_permute_csr_workspace_bytes(n),
                "permute workspace too small");
     cudaStream_t st = bh_cs(stream);
@@ -439,8 +489,28 @@ extern "C" int bh_permute_csr(const int64_t *row_ptr, const int32_t *col,
     k_set_last<<<1, 1, 0, st>>>(out_row_ptr, n, total);
     int grid = bh_blocks(n, 8);
     if (grid > kSMs * 32) grid = kSMs * 32;
-    k_permute_csr_fill<<<grid, 256, 0, st>>>(row_ptr, col, val, perm, rank, n,
-                                             out_row_ptr, out_col, out_val);
+    k_permute_csr_fill<V><<<grid, 256, 0, st>>>(row_ptr, col, val, perm, rank,
+                                                n, out_row_ptr, out_col, out_val);
     BH_CHECK_LAUNCH("k_permute_csr_fill");
     return BH_OK;
+}
+
+extern "C" int bh_permute_csr(const int64_t *row_ptr, const int32_t *col,
+                              const float *val, const int32_t *perm,
+                              const int32_t *rank, int64_t n,
+                              int64_t *out_row_ptr, int32_t *out_col,
+                              float *out_val, void *ws, size_t ws_bytes,
+                              bh_stream_t stream) {
+    return permute_impl(row_ptr, col, val, perm, rank, n, out_row_ptr, out_col,
+                        out_val, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_permute_csr_f64(const int64_t *row_ptr, const int32_t *col,
+                                  const double *val, const int32_t *perm,
+                                  const int32_t *rank, int64_t n,
+                                  int64_t *out_row_ptr, int32_t *out_col,
+                                  double *out_val, void *ws, size_t ws_bytes,
+                                  bh_stream_t stream) {
+    return permute_impl(row_ptr, col, val, perm, rank, n, out_row_ptr, out_col,
+                        out_val, ws, ws_bytes, stream);
 }

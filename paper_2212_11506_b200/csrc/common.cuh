@@ -74,9 +74,72 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T *smem, T *total) {
     return r;
 }
 
+// ---------------------------------------------------------------------------
+// Point precision (the reference's run dtype, io.py:21-30): T = float (f32
+// storage, f32 pair math) or double (f64 storage and arithmetic).
+// ---------------------------------------------------------------------------
+template <typename T> struct P2;
+template <> struct P2<float> { using type = float2; };
+template <> struct P2<double> { using type = double2; };
+template <typename T> using p2_t = typename P2<T>::type;
+
+template <typename T> __device__ __forceinline__ p2_t<T> mk2(T a, T b);
+template <> __device__ __forceinline__ float2 mk2<float>(float a, float b) {
+    return make_float2(a, b);
+}
+template <> __device__ __forceinline__ double2 mk2<double>(double a, double b) {
+    return make_double2(a, b);
+}
+
+// Node records (include/bhtsne_b200.h): f32 trees use one 16-B word
+// {com.x, com.y, mass, info}; f64 trees two, {com.x, com.y} (f64) then
+// {mass, info, 0, 0}.
+template <typename T> struct NodeRec;
+template <> struct NodeRec<float> {
+    static constexpr int kWords = 1;
+    __device__ static void store(void *base, int64_t i, float2 c, uint32_t m,
+                                 uint32_t info) {
+        ((float4 *)base)[i] = make_float4(c.x, c.y, __uint_as_float(m),
+                                          __uint_as_float(info));
+    }
+    __device__ static void store_info(void *base, int64_t i, uint32_t info) {
+        ((float4 *)base)[i].w = __uint_as_float(info);
+    }
+    __device__ static uint32_t info(const void *base, int64_t i) {
+        return __float_as_uint(((const float4 *)base)[i].w);
+    }
+    __device__ static uint32_t mass(const void *base, int64_t i) {
+        return __float_as_uint(((const float4 *)base)[i].z);
+    }
+    __device__ static float2 com(const void *base, int64_t i) {
+        const float4 r = ((const float4 *)base)[i];
+        return make_float2(r.x, r.y);
+    }
+};
+template <> struct NodeRec<double> {
+    static constexpr int kWords = 2;
+    __device__ static void store(void *base, int64_t i, double2 c, uint32_t m,
+                                 uint32_t info) {
+        ((double2 *)base)[2 * i] = c;
+        ((uint4 *)base)[2 * i + 1] = make_uint4(m, info, 0u, 0u);
+    }
+    __device__ static void store_info(void *base, int64_t i, uint32_t info) {
+        ((uint4 *)base)[2 * i + 1].y = info;
+    }
+    __device__ static uint32_t info(const void *base, int64_t i) {
+        return ((const uint4 *)base)[2 * i + 1].y;
+    }
+    __device__ static uint32_t mass(const void *base, int64_t i) {
+        return ((const uint4 *)base)[2 * i + 1].x;
+    }
+    __device__ static double2 com(const void *base, int64_t i) {
+        return ((const double2 *)base)[2 * i];
+    }
+};
+
 }  // namespace bh
 
-#define BH_CHECK_LAUNCH(what)                                                 \
+#define BH_CHECK_LAUNCH(what)                                           \
     do {                                                                      \
         cudaError_t e_ = cudaGetLastError();                                  \
         if (e_ != cudaSuccess) return bh::cuda_status(e_, what);              \

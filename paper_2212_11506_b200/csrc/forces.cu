@@ -3,7 +3,7 @@
 // the KL rows (optimizer.py:227-239).
 #include <algorithm>
 
-#include "common.cuh"
+#include "forces.cuh"
 
 namespace bh {
 
@@ -24,56 +24,6 @@ namespace bh {
 // Pair math is f32; contributions of one popped group are summed in f32 and
 // added to f64 accumulators.
 // ---------------------------------------------------------------------------
-constexpr int kRepWarps = 8;
-constexpr int kRepThreads = kRepWarps * 32;
-
-// Deterministic warp reduction: lane-strided sequential partials, then a
-// butterfly.  Called by one full warp; every lane returns the total.
-__device__ __forceinline__ double fixed_sum(const double *x, int64_t n) {
-    double s = 0.0;
-    for (int64_t i = threadIdx.x & 31; i < n; i += 32) s = __dadd_rn(s, __ldcg(&x[i]));
-    return warp_sum(s);
-}
-
-struct RepCounts {
-    int internal, leafnodes, leafpts, accepted;
-};
-
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-__device__ __forceinline__ int4 ld_stream_i4(const int32_t *p) {
-    int4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    return r;
-}
-
-__device__ __forceinline__ float4 ld_stream_f4(const float *p) {
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-    return r;
-}
-
-// Full-warp ballot; the traversal keeps the whole warp converged (every
-// branch is warp-uniform), so no divergence check is needed around it.
-__device__ __forceinline__ uint32_t ballot_full(bool p) {
-    uint32_t r;
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
-        "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t}"
-        : "=r"(r) : "r"((uint32_t)p));
-    return r;
-}
-
-struct Acc64 {
-    double z, r0, r1;
-};
-
 // Per-pop context of a lane: its point, the group's R2 and whether the lane
 // opened the node whose children are being visited.
 struct GroupCtx {
@@ -289,39 +239,8 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         if (A.zpart) A.zpart[o] = z;
         if (COUNT) A.counts[o] = make_int4(cn.internal, cn.leafnodes, cn.leafpts, cn.accepted);
     }
-    // Z: per-CTA partial (256 points in Morton order), then one fixed-order
-    // warp reduction over all CTA partials (fixed_sum) -- the same
-    // reduction the multi-GPU path applies to the gathered partials, so Z is
-    // bitwise independent of the GPU count.  No CTA-wide
-    // barrier: the last warp of the CTA to finish folds the warp partials.
-    const double wz = warp_sum(z);
-    unsigned last = 0;
-    if (lane == 0) {
-        s_z[warp] = wz;
-        __threadfence_block();
-        last = atomicAdd(&s_done, 1u) == kRepWarps - 1;
-    }
-    if (!__shfl_sync(0xffffffffu, last, 0)) return;
-    __threadfence_block();
-    if (lane == 0) {
-        double bz = 0.0;
-        for (int w = 0; w < kRepWarps; w++)
-            bz = __dadd_rn(bz, ((volatile double *)s_z)[w]);
-        zblock[bid] = bz;
-        if (A.z_out) {
-            __threadfence();
-            last = atomicAdd(A.ticket, 1u) == (unsigned)(nblk - 1);
-        } else {
-            last = 0;
-        }
-    }
-    if (!__shfl_sync(0xffffffffu, last, 0)) return;
-    __threadfence();
-    const double tot = fixed_sum(zblock, nblk);
-    if (lane == 0) {
-        *A.z_out = tot;
-        *A.ticket = 0;
-    }
+    rep_z_tail(z, warp, lane, bid, nblk, s_z, &s_done, zblock, A.ticket,
+               A.z_out);
 }
 
 template <int D, bool COUNT, bool QUERY>
@@ -513,9 +432,10 @@ k_repulsive_exact(const float2 *__restrict__ y, int64_t n,
 }
 
 // KL rows (optimizer.py:227-239) in f64, one warp per row.
+template <typename T>
 __global__ void __launch_bounds__(256)
 k_kl_rows(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-          const float *__restrict__ val, int64_t n, const float2 *__restrict__ y,
+          const T *__restrict__ val, int64_t n, const p2_t<T> *__restrict__ y,
           const double *__restrict__ zp, double *__restrict__ part,
           unsigned *__restrict__ ticket, double *__restrict__ kl_out) {
     __shared__ double s_a[8];
@@ -525,11 +445,11 @@ k_kl_rows(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
     double acc = 0.0;
     for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < n;
          row += (int64_t)gridDim.x * 8) {
-        const float2 yi = y[row];
+        const p2_t<T> yi = y[row];
         for (int64_t q = rp[row] + lane; q < rp[row + 1]; q += 32) {
-            const float p = val[q];
-            if (p == 0.0f) continue;  // padding
-            const float2 yj = y[col[q]];
+            const T p = val[q];
+            if (p == T(0)) continue;  // padding
+            const p2_t<T> yj = y[col[q]];
             double dx = (double)yi.x - (double)yj.x;
             double dy = (double)yi.y - (double)yj.y;
             double pd = (double)p;
@@ -556,7 +476,6 @@ k_kl_rows(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
     }
 }
 
-static int rep_grid(int64_t npts) { return bh_blocks(npts, kRepThreads); }
 
 }  // namespace bh
 
@@ -573,6 +492,7 @@ extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
                             double *z_out, int32_t *counts, void *ws,
                             size_t ws_bytes, bh_stream_t stream) {
     BH_REQUIRE(theta >= 0, "theta must be >= 0, got %g", theta);
+    BH_REQUIRE(t->precision != 64, "precision-64 tree: use the _f64 entry point");
     BH_REQUIRE(t_begin >= 0 && t_end <= t->n_points && t_begin <= t_end,
                "bad point range");
     if (t_end == t_begin) return BH_OK;
@@ -662,6 +582,7 @@ extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
                          float exaggeration, const bh_sched_t *sched,
                          float *attr, bh_stream_t stream) {
     BH_REQUIRE(theta >= 0, "theta must be >= 0, got %g", theta);
+    BH_REQUIRE(t->precision != 64, "precision-64 tree: use the _f64 entry point");
     BH_REQUIRE(t_begin >= 0 && t_end <= t->n_points && t_begin <= t_end,
                "bad point range");
     BH_REQUIRE(row_begin >= 0 && row_end <= n_rows && row_begin <= row_end,
@@ -739,18 +660,34 @@ extern "C" size_t bh_kl_workspace_bytes(int64_t n) {
     return bh_align(sizeof(double) * kSMs * 8) + 256;
 }
 
-extern "C" int bh_kl_rows(const int64_t *row_ptr, const int32_t *col,
-                          const float *val, int64_t n, int padded,
-                          const float *y, const double *z, double *kl_out,
-                          void *ws, size_t ws_bytes, bh_stream_t stream) {
-    (void)padded;  // pad entries carry p == 0 and are skipped
+template <typename T>
+static int kl_impl(const int64_t *row_ptr, const int32_t *col, const T *val,
+                   int64_t n, const T *y, const double *z, double *kl_out,
+                   void *ws, size_t ws_bytes, bh_stream_t stream) {
+    // pad entries carry p == 0 and are skipped
     BH_REQUIRE(ws_bytes >= bh_kl_workspace_bytes(n), "kl workspace too small");
     int grid = bh_blocks(n, 8);
     if (grid > kSMs * 8) grid = kSMs * 8;
     char *w = (char *)ws;
-    k_kl_rows<<<grid, 256, 0, bh_cs(stream)>>>(
-        row_ptr, col, val, n, (const float2 *)y, z, (double *)w,
+    k_kl_rows<T><<<grid, 256, 0, bh_cs(stream)>>>(
+        row_ptr, col, val, n, (const p2_t<T> *)y, z, (double *)w,
         (unsigned *)(w + bh_align(sizeof(double) * kSMs * 8)), kl_out);
     BH_CHECK_LAUNCH("k_kl_rows");
     return BH_OK;
+}
+
+extern "C" int bh_kl_rows(const int64_t *row_ptr, const int32_t *col,
+                          const float *val, int64_t n, int padded,
+                          const float *y, const double *z, double *kl_out,
+                          void *ws, size_t ws_bytes, bh_stream_t stream) {
+    (void)padded;
+    return kl_impl(row_ptr, col, val, n, y, z, kl_out, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_kl_rows_f64(const int64_t *row_ptr, const int32_t *col,
+                              const double *val, int64_t n, int padded,
+                              const double *y, const double *z, double *kl_out,
+                              void *ws, size_t ws_bytes, bh_stream_t stream) {
+    (void)padded;
+    return kl_impl(row_ptr, col, val, n, y, z, kl_out, ws, ws_bytes, stream);
 }

@@ -2,7 +2,8 @@
 // knn_exact (knn.py:36-73) with the reference's exact semantics: squared
 // distances accumulated in f64 over the columns in order (no FMA), k
 // smallest kept by strict-less insertion over ascending candidate ids (ties
-// -> lower id), self excluded, distances stored as float32.
+// -> lower id), self excluded, distances stored in the data's precision
+// (float32 data -> float32 distances; float64 data -> float64, knn.py:72).
 //
 // One thread per query, its row held in registers as f64; candidate rows are
 // staged per CTA in shared memory (f64, broadcast reads).  The partial sum
@@ -16,10 +17,10 @@ constexpr int kKnnThreads = 128;
 constexpr int kKnnTile = 32;
 constexpr int kKnnMaxK = 128;
 
-template <int DMAX>
+template <int DMAX, typename T>
 __global__ void __launch_bounds__(kKnnThreads)
-k_knn(const float *__restrict__ x, int64_t n, int d, int k,
-      int64_t *__restrict__ out_idx, float *__restrict__ out_sqd) {
+k_knn(const T *__restrict__ x, int64_t n, int d, int k,
+      int64_t *__restrict__ out_idx, T *__restrict__ out_sqd) {
     __shared__ double s_c[kKnnTile][DMAX];
     const int64_t i = blockIdx.x * (int64_t)kKnnThreads + threadIdx.x;
     const bool ok = i < n;
@@ -74,7 +75,7 @@ k_knn(const float *__restrict__ x, int64_t n, int d, int k,
     if (ok) {
         for (int t = 0; t < k; t++) {
             out_idx[i * k + t] = bi[t];
-            out_sqd[i * k + t] = __double2float_rn(bd[t]);
+            out_sqd[i * k + t] = (T)bd[t];
         }
     }
 }
@@ -83,8 +84,9 @@ k_knn(const float *__restrict__ x, int64_t n, int d, int k,
 
 using namespace bh;
 
-extern "C" int bh_knn(const float *x, int64_t n, int64_t d, int64_t k,
-                      int64_t *out_idx, float *out_sqd, bh_stream_t stream) {
+template <typename T>
+static int knn_impl(const T *x, int64_t n, int64_t d, int64_t k,
+                    int64_t *out_idx, T *out_sqd, bh_stream_t stream) {
     BH_REQUIRE(k >= 1 && k <= n - 1, "k must be in [1, %lld], got %lld",
                (long long)(n - 1), (long long)k);
     BH_REQUIRE(k <= kKnnMaxK, "k must be <= %d for bh_knn", kKnnMaxK);
@@ -93,11 +95,21 @@ extern "C" int bh_knn(const float *x, int64_t n, int64_t d, int64_t k,
     const int grid = bh_blocks(n, kKnnThreads);
     cudaStream_t st = bh_cs(stream);
     if (d <= 16)
-        k_knn<16><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
+        k_knn<16, T><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
     else if (d <= 32)
-        k_knn<32><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
+        k_knn<32, T><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
     else
-        k_knn<64><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
+        k_knn<64, T><<<grid, kKnnThreads, 0, st>>>(x, n, (int)d, (int)k, out_idx, out_sqd);
     BH_CHECK_LAUNCH("k_knn");
     return BH_OK;
+}
+
+extern "C" int bh_knn(const float *x, int64_t n, int64_t d, int64_t k,
+                      int64_t *out_idx, float *out_sqd, bh_stream_t stream) {
+    return knn_impl(x, n, d, k, out_idx, out_sqd, stream);
+}
+
+extern "C" int bh_knn_f64(const double *x, int64_t n, int64_t d, int64_t k,
+                          int64_t *out_idx, double *out_sqd, bh_stream_t stream) {
+    return knn_impl(x, n, d, k, out_idx, out_sqd, stream);
 }

@@ -7,6 +7,8 @@
 // the update uses explicit f32 intrinsics in numpy's (NEP 50) operation order.
 #include <float.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bh {
@@ -35,10 +37,12 @@ __device__ __forceinline__ uint64_t spread32(uint64_t m) {  // _spread_bits
 
 // compute_bounds (quadtree.py:145-153) from exact f32 extrema, plus the
 // Morton constants of _morton_kernel (quadtree.py:179-181).
-__device__ void finalize_bounds(float mn0, float mx0, float mn1, float mx1,
-                                int nonfinite, int code_bits, float sh0,
-                                float sh1, bh_bounds_t *out) {
-    double dmn0 = mn0, dmx0 = mx0, dmn1 = mn1, dmx1 = mx1;
+// Extrema arrive as f64 (exact for f32 points); sh*: the pending shift in
+// the run precision (f32 fields for f32 runs, f64 fields for f64 runs).
+__device__ void finalize_bounds(double dmn0, double dmx0, double dmn1,
+                                double dmx1, int nonfinite, int code_bits,
+                                float sh0, float sh1, double sh0d, double sh1d,
+                                bh_bounds_t *out) {
     double c0 = __dmul_rn(0.5, __dadd_rn(dmn0, dmx0));
     double c1 = __dmul_rn(0.5, __dadd_rn(dmn1, dmx1));
     double h0 = __dsub_rn(dmx0, c0), h1 = __dsub_rn(dmx1, c1);
@@ -60,49 +64,62 @@ __device__ void finalize_bounds(float mn0, float mx0, float mn1, float mx1,
     out->shift1 = sh1;
     out->nonfinite = nonfinite;
     out->code_bits = code_bits;
+    out->shift0_f64 = sh0d;
+    out->shift1_f64 = sh1d;
 }
 
+template <typename T>
 struct MinMax {
-    float mn0, mx0, mn1, mx1;
+    T mn0, mx0, mn1, mx1;
     int bad;
 };
 
-__device__ __forceinline__ void mm_init(MinMax &m) {
-    m.mn0 = m.mn1 = FLT_MAX;
-    m.mx0 = m.mx1 = -FLT_MAX;
+template <typename T> __device__ __forceinline__ T t_max();
+template <> __device__ __forceinline__ float t_max<float>() { return FLT_MAX; }
+template <> __device__ __forceinline__ double t_max<double>() { return DBL_MAX; }
+
+template <typename T>
+__device__ __forceinline__ void mm_init(MinMax<T> &m) {
+    m.mn0 = m.mn1 = t_max<T>();
+    m.mx0 = m.mx1 = -t_max<T>();
     m.bad = 0;
 }
 
-__device__ __forceinline__ void mm_add(MinMax &m, float a, float b) {
+template <typename T>
+__device__ __forceinline__ void mm_add(MinMax<T> &m, T a, T b) {
     if (!isfinite(a) || !isfinite(b)) m.bad = 1;
-    m.mn0 = fminf(m.mn0, a);
-    m.mx0 = fmaxf(m.mx0, a);
-    m.mn1 = fminf(m.mn1, b);
-    m.mx1 = fmaxf(m.mx1, b);
+    m.mn0 = fmin(m.mn0, a);
+    m.mx0 = fmax(m.mx0, a);
+    m.mn1 = fmin(m.mn1, b);
+    m.mx1 = fmax(m.mx1, b);
 }
 
-__device__ __forceinline__ void mm_warp(MinMax &m) {
+template <typename T>
+__device__ __forceinline__ void mm_warp(MinMax<T> &m) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        m.mn0 = fminf(m.mn0, __shfl_xor_sync(0xffffffffu, m.mn0, o));
-        m.mx0 = fmaxf(m.mx0, __shfl_xor_sync(0xffffffffu, m.mx0, o));
-        m.mn1 = fminf(m.mn1, __shfl_xor_sync(0xffffffffu, m.mn1, o));
-        m.mx1 = fmaxf(m.mx1, __shfl_xor_sync(0xffffffffu, m.mx1, o));
+        m.mn0 = fmin(m.mn0, __shfl_xor_sync(0xffffffffu, m.mn0, o));
+        m.mx0 = fmax(m.mx0, __shfl_xor_sync(0xffffffffu, m.mx0, o));
+        m.mn1 = fmin(m.mn1, __shfl_xor_sync(0xffffffffu, m.mn1, o));
+        m.mx1 = fmax(m.mx1, __shfl_xor_sync(0xffffffffu, m.mx1, o));
         m.bad |= __shfl_xor_sync(0xffffffffu, m.bad, o);
     }
 }
 
 // Block reduction of MinMax (and optionally two f64 sums); result valid in
 // thread 0.
+template <typename T>
 struct PtPartial {
-    float4 mm;
+    T mn0, mx0, mn1, mx1;
     double s0, s1;
     int bad;
     int pad;
 };
 
-__device__ void block_reduce(MinMax m, double s0, double s1, PtPartial *out) {
-    __shared__ MinMax sm[kPtThreads / 32];
+template <typename T>
+__device__ void block_reduce(MinMax<T> m, double s0, double s1,
+                             PtPartial<T> *out) {
+    __shared__ MinMax<T> sm[kPtThreads / 32];
     __shared__ double ss0[kPtThreads / 32], ss1[kPtThreads / 32];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     mm_warp(m);
@@ -115,18 +132,21 @@ __device__ void block_reduce(MinMax m, double s0, double s1, PtPartial *out) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        MinMax r = sm[0];
+        MinMax<T> r = sm[0];
         double a = ss0[0], b = ss1[0];
         for (int i = 1; i < kPtThreads / 32; i++) {
-            r.mn0 = fminf(r.mn0, sm[i].mn0);
-            r.mx0 = fmaxf(r.mx0, sm[i].mx0);
-            r.mn1 = fminf(r.mn1, sm[i].mn1);
-            r.mx1 = fmaxf(r.mx1, sm[i].mx1);
+            r.mn0 = fmin(r.mn0, sm[i].mn0);
+            r.mx0 = fmax(r.mx0, sm[i].mx0);
+            r.mn1 = fmin(r.mn1, sm[i].mn1);
+            r.mx1 = fmax(r.mx1, sm[i].mx1);
             r.bad |= sm[i].bad;
             a = __dadd_rn(a, ss0[i]);
             b = __dadd_rn(b, ss1[i]);
         }
-        out->mm = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+        out->mn0 = r.mn0;
+        out->mx0 = r.mx0;
+        out->mn1 = r.mn1;
+        out->mx1 = r.mx1;
         out->s0 = a;
         out->s1 = b;
         out->bad = r.bad;
@@ -147,60 +167,68 @@ __device__ bool last_block(unsigned *ticket) {
 // block: thread i folds partials i, i+blockDim, ... in order, then the same
 // fixed warp/block tree as block_reduce.  Deterministic for a given n (the
 // grid is a function of n).  Result valid in thread 0.
-__device__ PtPartial reduce_partials(const PtPartial *part, int nparts) {
-    MinMax m;
+template <typename T>
+__device__ PtPartial<T> reduce_partials(const PtPartial<T> *part, int nparts) {
+    MinMax<T> m;
     mm_init(m);
     double a = 0.0, b = 0.0;
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
-        float4 q = __ldcg(&part[i].mm);
-        m.mn0 = fminf(m.mn0, q.x);
-        m.mx0 = fmaxf(m.mx0, q.y);
-        m.mn1 = fminf(m.mn1, q.z);
-        m.mx1 = fmaxf(m.mx1, q.w);
+        m.mn0 = fmin(m.mn0, __ldcg(&part[i].mn0));
+        m.mx0 = fmax(m.mx0, __ldcg(&part[i].mx0));
+        m.mn1 = fmin(m.mn1, __ldcg(&part[i].mn1));
+        m.mx1 = fmax(m.mx1, __ldcg(&part[i].mx1));
         m.bad |= __ldcg(&part[i].bad);
         a = __dadd_rn(a, __ldcg(&part[i].s0));
         b = __dadd_rn(b, __ldcg(&part[i].s1));
     }
-    __shared__ PtPartial s_r;
+    __shared__ PtPartial<T> s_r;
     block_reduce(m, a, b, &s_r);
     __syncthreads();
     return s_r;
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kPtThreads)
-k_bounds(const float2 *__restrict__ y, int64_t n, int code_bits,
-         bh_bounds_t *out, PtPartial *part, unsigned *ticket) {
-    MinMax m;
+k_bounds(const p2_t<T> *__restrict__ y, int64_t n, int code_bits,
+         bh_bounds_t *out, PtPartial<T> *part, unsigned *ticket) {
+    MinMax<T> m;
     mm_init(m);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        float2 p = y[i];
+        const p2_t<T> p = y[i];
         mm_add(m, p.x, p.y);
     }
     block_reduce(m, 0.0, 0.0, &part[blockIdx.x]);
     if (!last_block(ticket)) return;
-    PtPartial r = reduce_partials(part, gridDim.x);
+    PtPartial<T> r = reduce_partials(part, gridDim.x);
     if (threadIdx.x == 0) {
-        finalize_bounds(r.mm.x, r.mm.y, r.mm.z, r.mm.w, r.bad, code_bits,
-                        0.0f, 0.0f, out);
+        finalize_bounds(r.mn0, r.mx0, r.mn1, r.mx1, r.bad, code_bits, 0.0f,
+                        0.0f, 0.0, 0.0, out);
         *ticket = 0;
     }
 }
 
-template <int BITS>
+// y - shift in the run precision (gradient_step's re-centering)
+__device__ __forceinline__ float2 shifted(float2 p, const bh_bounds_t *b) {
+    return make_float2(__fsub_rn(p.x, b->shift0), __fsub_rn(p.y, b->shift1));
+}
+__device__ __forceinline__ double2 shifted(double2 p, const bh_bounds_t *b) {
+    return make_double2(__dsub_rn(p.x, b->shift0_f64),
+                        __dsub_rn(p.y, b->shift1_f64));
+}
+
+template <int BITS, typename T>
 __global__ void __launch_bounds__(kPtThreads)
-k_morton(float2 *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
+k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
          int apply_shift,
          typename std::conditional<BITS == 32, uint32_t, uint64_t>::type
              *__restrict__ codes) {
     const double root0 = b->root0, root1 = b->root1, scale = b->scale;
-    const float sh0 = b->shift0, sh1 = b->shift1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        float2 p = y[i];
+        p2_t<T> p = y[i];
         if (apply_shift) {
-            p.x = __fsub_rn(p.x, sh0);
-            p.y = __fsub_rn(p.y, sh1);
+            p = shifted(p, b);
             y[i] = p;
         }
         double q0 = __dmul_rn(__dsub_rn((double)p.x, root0), scale);
@@ -221,6 +249,23 @@ __device__ __forceinline__ float sgnf(float x) {
 
 // One coordinate of _update_coord (optimizer.py:161-168) in numpy f32
 // semantics: every Python scalar is cast to float32, no FMA contraction.
+__device__ __forceinline__ double sgnd(double x) {
+    return (double)((x > 0.0) - (x < 0.0));
+}
+
+__device__ __forceinline__ void update_coord(double &y, double &v, double &g,
+                                             double grad, double mom,
+                                             double lr, double mg) {
+    // the same operations on float64 arrays (f64 run mode)
+    bool flip = sgnd(grad) != sgnd(v);
+    double gn = flip ? __dadd_rn(g, 0.2) : __dmul_rn(g, 0.8);
+    gn = gn < mg ? mg : gn;
+    g = gn;
+    double vn = __dsub_rn(__dmul_rn(mom, v), __dmul_rn(__dmul_rn(lr, gn), grad));
+    v = vn;
+    y = __dadd_rn(y, vn);
+}
+
 __device__ __forceinline__ void update_coord(float &y, float &v, float &g,
                                              float grad, float mom, float lr,
                                              float mg) {
@@ -233,33 +278,66 @@ __device__ __forceinline__ void update_coord(float &y, float &v, float &g,
     y = __fadd_rn(y, vn);
 }
 
+// Schedule constants and gradient in the run precision: f32 runs use the
+// f32 fields and f32(Z) (numpy's weak-scalar promotion of rep / z on f32
+// arrays), f64 runs the f64 fields and Z itself.
+struct SchedF32 {
+    float z, mom, lr, mg;
+    __device__ void init(const bh_sched_t *s, int it) {
+        z = __double2float_rn(s->z);
+        mom = it < s->momentum_switch ? s->momentum_early : s->momentum_late;
+        lr = s->learning_rate;
+        mg = s->min_gain;
+    }
+    __device__ float grad(float a, float r) const {
+        return __fmul_rn(4.0f, __fsub_rn(a, __fdiv_rn(r, z)));
+    }
+};
+struct SchedF64 {
+    double z, mom, lr, mg;
+    __device__ void init(const bh_sched_t *s, int it) {
+        z = s->z;
+        mom = it < s->momentum_switch ? s->momentum_early_f64
+                                      : s->momentum_late_f64;
+        lr = s->learning_rate_f64;
+        mg = s->min_gain_f64;
+    }
+    __device__ double grad(double a, double r) const {
+        return __dmul_rn(4.0, __dsub_rn(a, __ddiv_rn(r, z)));
+    }
+};
+template <typename T>
+using sched_t = typename std::conditional<std::is_same<T, float>::value,
+                                          SchedF32, SchedF64>::type;
+
+__device__ __forceinline__ float fsub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double fsub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
 __global__ void __launch_bounds__(kPtThreads)
-k_update(float2 *__restrict__ y, float2 *__restrict__ v,
-         float2 *__restrict__ g, const float2 *__restrict__ attr,
-         const float2 *__restrict__ rep, const int32_t *__restrict__ rep_rank,
+k_update(p2_t<T> *__restrict__ y, p2_t<T> *__restrict__ v,
+         p2_t<T> *__restrict__ g, const p2_t<T> *__restrict__ attr,
+         const p2_t<T> *__restrict__ rep, const int32_t *__restrict__ rep_rank,
          int64_t n, bh_sched_t *sched, bh_bounds_t *out, int code_bits,
-         PtPartial *part, unsigned *ticket) {
+         PtPartial<T> *part, unsigned *ticket) {
     const int it = sched->iteration;
-    const float zf = __double2float_rn(sched->z);
-    const float mom = it < sched->momentum_switch ? sched->momentum_early
-                                                  : sched->momentum_late;
-    const float lr = sched->learning_rate, mg = sched->min_gain;
-    MinMax m;
+    sched_t<T> S;
+    S.init(sched, it);
+    MinMax<T> m;
     mm_init(m);
     double s0 = 0.0, s1 = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        float2 a = attr[i], r = rep[rep_rank ? (int64_t)rep_rank[i] : i];
+        const p2_t<T> a = attr[i], r = rep[rep_rank ? (int64_t)rep_rank[i] : i];
         // grad = 4.0 * (attr - rep / z)   (optimizer.py:205-207)
-        float gx = __fmul_rn(4.0f, __fsub_rn(a.x, __fdiv_rn(r.x, zf)));
-        float gy = __fmul_rn(4.0f, __fsub_rn(a.y, __fdiv_rn(r.y, zf)));
+        const T gx = S.grad(a.x, r.x), gy = S.grad(a.y, r.y);
         if (!isfinite(gx) || !isfinite(gy))
             atomicMin((unsigned long long *)&sched->bad,
                       ((unsigned long long)(unsigned)it << 32) |
                           (unsigned long long)i);
-        float2 yy = y[i], vv = v[i], gg = g[i];
-        update_coord(yy.x, vv.x, gg.x, gx, mom, lr, mg);
-        update_coord(yy.y, vv.y, gg.y, gy, mom, lr, mg);
+        p2_t<T> yy = y[i], vv = v[i], gg = g[i];
+        update_coord(yy.x, vv.x, gg.x, gx, S.mom, S.lr, S.mg);
+        update_coord(yy.y, vv.y, gg.y, gy, S.mom, S.lr, S.mg);
         y[i] = yy;
         v[i] = vv;
         g[i] = gg;
@@ -269,31 +347,29 @@ k_update(float2 *__restrict__ y, float2 *__restrict__ v,
     }
     block_reduce(m, s0, s1, &part[blockIdx.x]);
     if (!last_block(ticket)) return;
-    PtPartial r = reduce_partials(part, gridDim.x);
+    PtPartial<T> r = reduce_partials(part, gridDim.x);
     if (threadIdx.x == 0) {
-        // y -= f32(mean_f64(y))   (optimizer.py:220-221); rounding is
-        // monotone, so min(y - m) == f32(min(y) - m): the bounds of the
+        // y -= T(mean_f64(y))   (optimizer.py:220-221); rounding is
+        // monotone, so min(y - m) == rn(min(y) - m): the bounds of the
         // re-centred cloud come straight from the extrema.
-        float m0 = __double2float_rn(__ddiv_rn(r.s0, (double)n));
-        float m1 = __double2float_rn(__ddiv_rn(r.s1, (double)n));
-        finalize_bounds(__fsub_rn(r.mm.x, m0), __fsub_rn(r.mm.y, m0),
-                        __fsub_rn(r.mm.z, m1), __fsub_rn(r.mm.w, m1), r.bad,
-                        code_bits, m0, m1, out);
+        const double d0 = __ddiv_rn(r.s0, (double)n);
+        const double d1 = __ddiv_rn(r.s1, (double)n);
+        const T m0 = (T)d0, m1 = (T)d1;
+        finalize_bounds(fsub_rn(r.mn0, m0), fsub_rn(r.mx0, m0),
+                        fsub_rn(r.mn1, m1), fsub_rn(r.mx1, m1), r.bad,
+                        code_bits, (float)m0, (float)m1, (double)m0,
+                        (double)m1, out);
         sched->iteration = it + 1;
         *ticket = 0;
     }
 }
 
-__global__ void k_center(float2 *__restrict__ y, int64_t n,
+template <typename T>
+__global__ void k_center(p2_t<T> *__restrict__ y, int64_t n,
                          const bh_bounds_t *__restrict__ b) {
-    const float sh0 = b->shift0, sh1 = b->shift1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        float2 p = y[i];
-        p.x = __fsub_rn(p.x, sh0);
-        p.y = __fsub_rn(p.y, sh1);
-        y[i] = p;
-    }
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = shifted(y[i], b);
 }
 
 static int pt_grid(int64_t n) {
@@ -302,7 +378,60 @@ static int pt_grid(int64_t n) {
 }
 
 static size_t pt_ws_bytes(int64_t n) {
-    return bh_align(sizeof(PtPartial) * pt_grid(n)) + 256;
+    return bh_align(sizeof(PtPartial<double>) * pt_grid(n)) + 256;
+}
+
+template <typename T>
+static int bounds_impl(const T *y, int64_t n, int code_bits, bh_bounds_t *out,
+                       void *ws, size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(n >= 1, "need at least one point");
+    BH_REQUIRE(code_bits == 32 || code_bits == 64, "code_bits must be 32 or 64");
+    BH_REQUIRE(ws_bytes >= pt_ws_bytes(n), "bounds workspace too small");
+    int grid = pt_grid(n);
+    char *w = (char *)ws;
+    PtPartial<T> *part = (PtPartial<T> *)w;
+    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial<T>) * grid));
+    k_bounds<T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
+        (const p2_t<T> *)y, n, code_bits, out, part, ticket);
+    BH_CHECK_LAUNCH("k_bounds");
+    return BH_OK;
+}
+
+template <typename T>
+static int morton_impl(T *y, int64_t n, const bh_bounds_t *bounds,
+                       int code_bits, int apply_shift, void *codes,
+                       bh_stream_t stream) {
+    BH_REQUIRE(n >= 1, "need at least one point");
+    int grid = pt_grid(n);
+    if (code_bits == 32)
+        k_morton<32, T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
+            (p2_t<T> *)y, n, bounds, apply_shift, (uint32_t *)codes);
+    else if (code_bits == 64)
+        k_morton<64, T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
+            (p2_t<T> *)y, n, bounds, apply_shift, (uint64_t *)codes);
+    else
+        return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
+    BH_CHECK_LAUNCH("k_morton");
+    return BH_OK;
+}
+
+template <typename T>
+static int update_impl(T *y, T *v, T *g, const T *attr, const T *rep,
+                       const int32_t *rep_rank, int64_t n, bh_sched_t *sched,
+                       bh_bounds_t *bounds_out, int code_bits, void *ws,
+                       size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(n >= 1, "need at least one point");
+    BH_REQUIRE(ws_bytes >= pt_ws_bytes(n), "update workspace too small");
+    int grid = pt_grid(n);
+    char *w = (char *)ws;
+    PtPartial<T> *part = (PtPartial<T> *)w;
+    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial<T>) * grid));
+    k_update<T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
+        (p2_t<T> *)y, (p2_t<T> *)v, (p2_t<T> *)g, (const p2_t<T> *)attr,
+        (const p2_t<T> *)rep, rep_rank, n, sched, bounds_out, code_bits, part,
+        ticket);
+    BH_CHECK_LAUNCH("k_update");
+    return BH_OK;
 }
 
 }  // namespace bh
@@ -315,60 +444,58 @@ extern "C" size_t bh_update_workspace_bytes(int64_t n) { return pt_ws_bytes(n); 
 extern "C" int bh_bounds(const float *y, int64_t n, int code_bits,
                          bh_bounds_t *out, void *ws, size_t ws_bytes,
                          bh_stream_t stream) {
-    BH_REQUIRE(n >= 1, "need at least one point");
-    BH_REQUIRE(code_bits == 32 || code_bits == 64, "code_bits must be 32 or 64");
-    BH_REQUIRE(ws_bytes >= pt_ws_bytes(n), "bounds workspace too small");
-    int grid = pt_grid(n);
-    char *w = (char *)ws;
-    PtPartial *part = (PtPartial *)w;
-    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial) * grid));
-    k_bounds<<<grid, kPtThreads, 0, bh_cs(stream)>>>((const float2 *)y, n,
-                                                     code_bits, out, part,
-                                                     ticket);
-    BH_CHECK_LAUNCH("k_bounds");
-    return BH_OK;
+    return bounds_impl(y, n, code_bits, out, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_bounds_f64(const double *y, int64_t n, int code_bits,
+                             bh_bounds_t *out, void *ws, size_t ws_bytes,
+                             bh_stream_t stream) {
+    return bounds_impl(y, n, code_bits, out, ws, ws_bytes, stream);
 }
 
 extern "C" int bh_morton(float *y, int64_t n, const bh_bounds_t *bounds,
                          int code_bits, int apply_shift, void *codes,
                          bh_stream_t stream) {
-    BH_REQUIRE(n >= 1, "need at least one point");
-    int grid = pt_grid(n);
-    if (code_bits == 32)
-        k_morton<32><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
-            (float2 *)y, n, bounds, apply_shift, (uint32_t *)codes);
-    else if (code_bits == 64)
-        k_morton<64><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
-            (float2 *)y, n, bounds, apply_shift, (uint64_t *)codes);
-    else
-        return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
-    BH_CHECK_LAUNCH("k_morton");
-    return BH_OK;
+    return morton_impl(y, n, bounds, code_bits, apply_shift, codes, stream);
+}
+
+extern "C" int bh_morton_f64(double *y, int64_t n, const bh_bounds_t *bounds,
+                             int code_bits, int apply_shift, void *codes,
+                             bh_stream_t stream) {
+    return morton_impl(y, n, bounds, code_bits, apply_shift, codes, stream);
 }
 
 extern "C" int bh_update(float *y, float *v, float *g, const float *attr,
                          const float *rep, const int32_t *rep_rank, int64_t n,
-                         bh_sched_t *sched,
-                         bh_bounds_t *bounds_out, int code_bits, void *ws,
-                         size_t ws_bytes, bh_stream_t stream) {
-    BH_REQUIRE(n >= 1, "need at least one point");
-    BH_REQUIRE(ws_bytes >= pt_ws_bytes(n), "update workspace too small");
-    int grid = pt_grid(n);
-    char *w = (char *)ws;
-    PtPartial *part = (PtPartial *)w;
-    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial) * grid));
-    k_update<<<grid, kPtThreads, 0, bh_cs(stream)>>>(
-        (float2 *)y, (float2 *)v, (float2 *)g, (const float2 *)attr,
-        (const float2 *)rep, rep_rank, n, sched, bounds_out, code_bits, part,
-        ticket);
-    BH_CHECK_LAUNCH("k_update");
-    return BH_OK;
+                         bh_sched_t *sched, bh_bounds_t *bounds_out,
+                         int code_bits, void *ws, size_t ws_bytes,
+                         bh_stream_t stream) {
+    return update_impl(y, v, g, attr, rep, rep_rank, n, sched, bounds_out,
+                       code_bits, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_update_f64(double *y, double *v, double *g,
+                             const double *attr, const double *rep,
+                             const int32_t *rep_rank, int64_t n,
+                             bh_sched_t *sched, bh_bounds_t *bounds_out,
+                             int code_bits, void *ws, size_t ws_bytes,
+                             bh_stream_t stream) {
+    return update_impl(y, v, g, attr, rep, rep_rank, n, sched, bounds_out,
+                       code_bits, ws, ws_bytes, stream);
 }
 
 extern "C" int bh_center(float *y, int64_t n, const bh_bounds_t *bounds,
                          bh_stream_t stream) {
-    k_center<<<pt_grid(n), kPtThreads, 0, bh_cs(stream)>>>((float2 *)y, n,
-                                                           bounds);
+    k_center<float><<<pt_grid(n), kPtThreads, 0, bh_cs(stream)>>>(
+        (float2 *)y, n, bounds);
+    BH_CHECK_LAUNCH("k_center");
+    return BH_OK;
+}
+
+extern "C" int bh_center_f64(double *y, int64_t n, const bh_bounds_t *bounds,
+                             bh_stream_t stream) {
+    k_center<double><<<pt_grid(n), kPtThreads, 0, bh_cs(stream)>>>(
+        (double2 *)y, n, bounds);
     BH_CHECK_LAUNCH("k_center");
     return BH_OK;
 }
@@ -411,8 +538,10 @@ extern "C" int bh_gather_rows(const void *src, const int32_t *idx, int64_t n,
         k_gather<uint32_t><<<grid, kPtThreads, 0, st>>>((const uint32_t *)src, idx, n, (uint32_t *)dst);
     else if (elem_bytes == 8)
         k_gather<uint2><<<grid, kPtThreads, 0, st>>>((const uint2 *)src, idx, n, (uint2 *)dst);
+    else if (elem_bytes == 16)
+        k_gather<uint4><<<grid, kPtThreads, 0, st>>>((const uint4 *)src, idx, n, (uint4 *)dst);
     else
-        return set_error(BH_ERR_ARG, "elem_bytes must be 4 or 8");
+        return set_error(BH_ERR_ARG, "elem_bytes must be 4, 8 or 16");
     BH_CHECK_LAUNCH("k_gather");
     return BH_OK;
 }
@@ -425,8 +554,10 @@ extern "C" int bh_scatter_rows(const void *src, const int32_t *idx, int64_t n,
         k_scatter<uint32_t><<<grid, kPtThreads, 0, st>>>((const uint32_t *)src, idx, n, (uint32_t *)dst);
     else if (elem_bytes == 8)
         k_scatter<uint2><<<grid, kPtThreads, 0, st>>>((const uint2 *)src, idx, n, (uint2 *)dst);
+    else if (elem_bytes == 16)
+        k_scatter<uint4><<<grid, kPtThreads, 0, st>>>((const uint4 *)src, idx, n, (uint4 *)dst);
     else
-        return set_error(BH_ERR_ARG, "elem_bytes must be 4 or 8");
+        return set_error(BH_ERR_ARG, "elem_bytes must be 4, 8 or 16");
     BH_CHECK_LAUNCH("k_scatter");
     return BH_OK;
 }

@@ -115,15 +115,16 @@ k_tree_scan(const uint32_t *__restrict__ blk_counts, int nblk,
     }
 }
 
-template <typename K, int D>
+template <typename K, int D, typename T>
 __global__ void __launch_bounds__(kTreeThreads)
 k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
-            const float2 *__restrict__ y, int64_t n,
+            const p2_t<T> *__restrict__ y, int64_t n,
             const uint32_t *__restrict__ blk_off,
-            const int32_t *__restrict__ level_off, float4 *__restrict__ node,
+            const int32_t *__restrict__ level_off, void *__restrict__ node,
             int32_t *__restrict__ parent, int32_t *__restrict__ node_start,
-            int32_t *__restrict__ leaf_end, float2 *__restrict__ ys,
+            int32_t *__restrict__ leaf_end, p2_t<T> *__restrict__ ys,
             int32_t *__restrict__ rank, const int32_t *__restrict__ status) {
+    using Rec = NodeRec<T>;
     if (*status != BH_OK) return;
     __shared__ uint32_t s_bal[kTreeWarps][D + 1];
     __shared__ uint32_t s_woff[kTreeWarps][D + 1];
@@ -167,7 +168,7 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
                        __popc(s_bal[warp][d] & lt);
             };
             const int32_t pid = order[t];
-            const float2 p = y[pid];
+            const p2_t<T> p = y[pid];
             ys[t] = p;
             if (rank) rank[pid] = (int32_t)t;
             for (int d = lo; d <= hi; d++) {
@@ -176,15 +177,14 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
                 parent[id] = d == 0 ? -1 : (d == lo ? base(d - 1) - 1 : base(d - 1));
                 node_start[id] = (int32_t)t;
                 if (!leaf) {
-                    node[id].w = __uint_as_float((uint32_t)base(d + 1));
+                    Rec::store_info(node, id, (uint32_t)base(d + 1));
                 } else if (s1 < D) {
                     // single-point leaf: complete record (quadtree.py:490-498)
-                    node[id] = make_float4(p.x, p.y, __uint_as_float(1u),
-                                           __uint_as_float(BH_LEAF_BIT | (uint32_t)t));
+                    Rec::store(node, id, p, 1u, BH_LEAF_BIT | (uint32_t)t);
                     leaf_end[id] = (int32_t)(t + 1);
                 } else {
                     // first point of a run of equal codes (depth-D bucket)
-                    node[id].w = __uint_as_float(BH_LEAF_BIT | (uint32_t)t);
+                    Rec::store_info(node, id, BH_LEAF_BIT | (uint32_t)t);
                 }
             }
             // last point of a run of equal codes closes its depth-D leaf
@@ -198,18 +198,20 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
 // the consecutive level-(d+1) nodes with parent == node (at most 4);
 // mass = sum, com = sum(m_ch * f64(com_ch)) / m in child order.  Leaves
 // still open here are depth-D buckets: f64 mean of their points in order.
+template <typename T>
 __global__ void __launch_bounds__(kSumThreads)
-k_summarize_level(float4 *__restrict__ node, const int32_t *__restrict__ parent,
+k_summarize_level(void *__restrict__ node, const int32_t *__restrict__ parent,
                   const int32_t *__restrict__ leaf_end,
-                  const float2 *__restrict__ ys,
+                  const p2_t<T> *__restrict__ ys,
                   const int32_t *__restrict__ level_off, int d, int D,
                   const int32_t *__restrict__ status) {
+    using Rec = NodeRec<T>;
     if (*status != BH_OK) return;
     const int32_t lo = level_off[d], hi = level_off[d + 1];
     const int32_t hi_next = d < D ? level_off[d + 2] : hi;
     for (int32_t nd = lo + blockIdx.x * kSumThreads + threadIdx.x; nd < hi;
          nd += gridDim.x * kSumThreads) {
-        const uint32_t info = __float_as_uint(node[nd].w);
+        const uint32_t info = Rec::info(node, nd);
         if (info & BH_LEAF_BIT) {
             if (d < D) continue;  // single-point leaf, completed by emit
             const uint32_t t = info & ~BH_LEAF_BIT;
@@ -218,13 +220,14 @@ k_summarize_level(float4 *__restrict__ node, const int32_t *__restrict__ parent,
             if (cnt == 1) continue;  // completed by emit
             double a = 0.0, b = 0.0;
             for (int64_t q = t; q < end; q++) {
-                const float2 p = ys[q];
+                const p2_t<T> p = ys[q];
                 a = __dadd_rn(a, (double)p.x);
                 b = __dadd_rn(b, (double)p.y);
             }
-            node[nd] = make_float4(__double2float_rn(__ddiv_rn(a, (double)cnt)),
-                                   __double2float_rn(__ddiv_rn(b, (double)cnt)),
-                                   __uint_as_float(cnt), __uint_as_float(info));
+            Rec::store(node, nd,
+                       mk2<T>((T)__ddiv_rn(a, (double)cnt),
+                              (T)__ddiv_rn(b, (double)cnt)),
+                       cnt, info);
             continue;
         }
         const uint32_t fc = info & BH_CHILD_MASK;
@@ -233,18 +236,17 @@ k_summarize_level(float4 *__restrict__ node, const int32_t *__restrict__ parent,
 #pragma unroll
         for (uint32_t c = 0; c < 4; c++) {
             if ((int32_t)(fc + c) < hi_next && parent[fc + c] == nd) {
-                const float4 r = node[fc + c];
-                const uint32_t mc = __float_as_uint(r.z);
+                const p2_t<T> cc = Rec::com(node, fc + c);
+                const uint32_t mc = Rec::mass(node, fc + c);
                 m += mc;
-                a = __dadd_rn(a, __dmul_rn((double)mc, (double)r.x));
-                b = __dadd_rn(b, __dmul_rn((double)mc, (double)r.y));
+                a = __dadd_rn(a, __dmul_rn((double)mc, (double)cc.x));
+                b = __dadd_rn(b, __dmul_rn((double)mc, (double)cc.y));
                 k = c + 1;
             }
         }
-        node[nd] = make_float4(__double2float_rn(__ddiv_rn(a, (double)m)),
-                               __double2float_rn(__ddiv_rn(b, (double)m)),
-                               __uint_as_float(m),
-                               __uint_as_float(fc | ((k - 1) << BH_NKIDS_SHIFT)));
+        Rec::store(node, nd,
+                   mk2<T>((T)__ddiv_rn(a, (double)m), (T)__ddiv_rn(b, (double)m)),
+                   m, fc | ((k - 1) << BH_NKIDS_SHIFT));
     }
 }
 
@@ -263,8 +265,8 @@ static TreeLayout tree_layout(int64_t n, int D) {
     return L;
 }
 
-template <typename K, int D>
-static int build_impl(const bh_tree_t *t, const float *y, void *ws,
+template <typename K, int D, typename T>
+static int build_impl(const bh_tree_t *t, const void *y, void *ws,
                       cudaStream_t st) {
     TreeLayout L = tree_layout(t->n_points, D);
     char *w = (char *)ws;
@@ -275,10 +277,10 @@ static int build_impl(const bh_tree_t *t, const float *y, void *ws,
     k_tree_scan<D><<<1, 1024, 0, st>>>(cnt, L.nblk, off, t->level_off,
                                        t->node_capacity, t->status);
     BH_CHECK_LAUNCH("k_tree_scan");
-    k_tree_emit<K, D><<<L.nblk, kTreeThreads, 0, st>>>(
-        sc, t->order, (const float2 *)y, t->n_points, off, t->level_off,
-        (float4 *)t->node, t->parent, t->node_start, t->leaf_end,
-        (float2 *)t->ys, t->rank, t->status);
+    k_tree_emit<K, D, T><<<L.nblk, kTreeThreads, 0, st>>>(
+        sc, t->order, (const p2_t<T> *)y, t->n_points, off, t->level_off,
+        (void *)t->node, t->parent, t->node_start, t->leaf_end,
+        (p2_t<T> *)t->ys, t->rank, t->status);
     BH_CHECK_LAUNCH("k_tree_emit");
     return BH_OK;
 }
@@ -291,14 +293,23 @@ extern "C" size_t bh_tree_workspace_bytes(int64_t n, int code_bits) {
     return tree_layout(n, code_bits / 2).total;
 }
 
-extern "C" int bh_build_tree(const bh_tree_t *t, const float *y, void *ws,
+static bool tree_f64(const bh_tree_t *t) { return t->precision == 64; }
+
+extern "C" int bh_build_tree(const bh_tree_t *t, const void *y, void *ws,
                              size_t ws_bytes, bh_stream_t stream) {
     BH_REQUIRE(t && t->n_points >= 1, "need at least one point");
     BH_REQUIRE(t->n_points < (int64_t)0x7fffffff, "too many points");
     BH_REQUIRE(ws_bytes >= bh_tree_workspace_bytes(t->n_points, t->code_bits),
                "tree workspace too small");
-    if (t->code_bits == 32) return build_impl<uint32_t, 16>(t, y, ws, bh_cs(stream));
-    if (t->code_bits == 64) return build_impl<uint64_t, 32>(t, y, ws, bh_cs(stream));
+    BH_REQUIRE(t->precision == 0 || t->precision == 32 || t->precision == 64,
+               "precision must be 32 or 64, got %d", t->precision);
+    cudaStream_t st = bh_cs(stream);
+    if (t->code_bits == 32)
+        return tree_f64(t) ? build_impl<uint32_t, 16, double>(t, y, ws, st)
+                           : build_impl<uint32_t, 16, float>(t, y, ws, st);
+    if (t->code_bits == 64)
+        return tree_f64(t) ? build_impl<uint64_t, 32, double>(t, y, ws, st)
+                           : build_impl<uint64_t, 32, float>(t, y, ws, st);
     return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
 }
 
@@ -319,9 +330,14 @@ extern "C" int bh_summarize(const bh_tree_t *t, void *ws, size_t ws_bytes,
     int grid = bh_blocks(t->n_points, kSumThreads);
     if (grid > max_blocks) grid = max_blocks;
     for (int d = D; d >= 0; d--) {
-        k_summarize_level<<<grid, kSumThreads, 0, bh_cs(stream)>>>(
-            (float4 *)t->node, t->parent, t->leaf_end, (const float2 *)t->ys,
-            t->level_off, d, D, t->status);
+        if (tree_f64(t))
+            k_summarize_level<double><<<grid, kSumThreads, 0, bh_cs(stream)>>>(
+                (void *)t->node, t->parent, t->leaf_end,
+                (const double2 *)t->ys, t->level_off, d, D, t->status);
+        else
+            k_summarize_level<float><<<grid, kSumThreads, 0, bh_cs(stream)>>>(
+                (void *)t->node, t->parent, t->leaf_end, (const float2 *)t->ys,
+                t->level_off, d, D, t->status);
         BH_CHECK_LAUNCH("k_summarize_level");
     }
     return BH_OK;

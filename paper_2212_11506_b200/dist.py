@@ -75,7 +75,7 @@ class Shard:
         self.plan = ShardPlan(eng.n, self.world, self.rank)
         pl = self.plan
         dev = eng.dev
-        f32 = dict(dtype=torch.float32, device=dev)
+        f32 = dict(dtype=eng.dtype, device=dev)  # the run precision
         self.attr_send = torch.zeros((pl.chunk, 2), **f32)
         self.rep_send = torch.zeros((pl.chunk, 2), **f32)
         self.z_send = torch.zeros(pl.partials_per_rank, dtype=torch.float64,
@@ -105,13 +105,14 @@ class Shard:
         r0, r1 = self.plan.mine
         y = eng.y  # storage order (see Engine.relabel)
         # attr[row] for rows [r0, r1) lands at attr_send[row - r0]
-        base = C.c_void_p(self.attr_send.data_ptr() - 8 * r0)
-        call("bh_attractive", ptr(eng.rp), ptr(eng.col), ptr(eng.val), eng.n,
-             1, ptr(y), r0, r1, 1.0, ptr(eng.sched), base, st)
+        base = C.c_void_p(self.attr_send.data_ptr() - eng.pt_bytes * r0)
+        call(eng.fn("bh_attractive"), ptr(eng.rp), ptr(eng.col), ptr(eng.val),
+             eng.n, 1, ptr(y), r0, r1, 1.0, ptr(eng.sched), base, st)
         rec(3)
-        call("bh_repulsive", eng.tree.sref(), ptr(eng.bounds), eng.theta, None,
-             r0, r1, 1, ptr(self.rep_send), None, ptr(self.z_send), None, None,
-             ptr(eng.ws_rep), eng.ws_rep.numel(), st)
+        call(eng.fn("bh_repulsive"), eng.tree.sref(), ptr(eng.bounds),
+             eng.theta, None, r0, r1, 1, ptr(self.rep_send), None,
+             ptr(self.z_send), None, None, ptr(eng.ws_rep),
+             eng.ws_rep.numel(), st)
         rec(4)
         self._gather()
         call("bh_sum_partials", ptr(self.z_all), self.z_all.numel(),

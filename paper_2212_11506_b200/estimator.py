@@ -50,7 +50,7 @@ class BarnesHutTSNE:
 
     def fit_transform(self, x, knn=None) -> np.ndarray:
         """Embed an N x D matrix into N x 2 (estimator.ts:57-98)."""
-        data = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+        data = np.ascontiguousarray(np.asarray(x, dtype=self.config.dtype))
         if data.ndim != 2:
             raise ValueError(f"expected a 2-D matrix, got {data.ndim}-D")
         if data.shape[0] < 2:

@@ -3,8 +3,14 @@
 Mirrors bhtsne.forces (reference: pkg/src/bhtsne/forces.py):
 ``GradientBuffers`` (:30-53), ``attractive`` (:56-82), ``repulsive_bh``
 (:85-150) and ``repulsive_exact`` (:153-182), with the same argument
-meaning and error messages.  Buffers are (N, 2) float32 / (N,) float64
-CUDA tensors; ``z`` is kept on the device and read on access.
+meaning and error messages.  Buffers are (N, 2) float32 or float64 / (N,)
+float64 CUDA tensors; ``z`` is kept on the device and read on access.
+
+Precision: as in the reference, the arrays' dtype selects it -- float64
+points (or a float64 P / tree) run the library's ``_f64`` kernels, whose
+pair terms are float64 in the reference's operation order; float32 runs
+the f32 kernels (f32 pair terms, f64 accumulation).  Mixed inputs are
+promoted to float64 (exact), the reference's own arithmetic.
 """
 
 from __future__ import annotations
@@ -23,21 +29,23 @@ from .quadtree import MortonQuadtree, as_points
 class GradientBuffers:
     """Per-point force accumulators and the normalisation term Z."""
 
-    attr: torch.Tensor       # (N, 2) float32
-    rep: torch.Tensor        # (N, 2) float32, unnormalised repulsion
+    attr: torch.Tensor       # (N, 2) float32 | float64
+    rep: torch.Tensor        # (N, 2), unnormalised repulsion
     z_partial: torch.Tensor  # (N,) float64 per-point contributions to Z
     z_dev: torch.Tensor = field(default=None)  # (1,) float64 on device
 
     @classmethod
     def allocate(cls, n: int, dtype=np.float32) -> "GradientBuffers":
-        if np.dtype(dtype) != np.float32:
-            raise ValueError("the B200 path computes in float32 (precision "
-                             "'f32'); float64 buffers are not supported")
+        dt = _lib.torch_dtype(dtype)
         dev = _lib.device()
-        f = lambda: torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        f = lambda: torch.zeros((n, 2), dtype=dt, device=dev)
         return cls(attr=f(), rep=f(),
                    z_partial=torch.zeros(n, dtype=torch.float64, device=dev),
                    z_dev=torch.zeros(1, dtype=torch.float64, device=dev))
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.attr.dtype
 
     @property
     def z(self) -> float:
@@ -49,15 +57,26 @@ class GradientBuffers:
     rep1 = property(lambda s: s.rep[:, 1])
 
 
+def _check_out(out: GradientBuffers, dt: torch.dtype, what: str):
+    if out.dtype != dt:
+        raise ValueError(f"{what}: buffers are {out.dtype}, the inputs run in "
+                         f"{dt} (allocate GradientBuffers with that dtype)")
+
+
 def attractive(p, y, out: GradientBuffers) -> None:
     """attr_i = sum_j p_ij (y_i - y_j) / (1 + |y_i - y_j|^2) -- forces.py:56."""
     pts = as_points(y)
     n = pts.shape[0]
     if p.n != n:
         raise ValueError(f"matrix is over {p.n} points, embedding has {n}")
-    call("bh_attractive", ptr(p.row_offsets), ptr(p.col_indices),
-         ptr(p.base_values), n, 0, ptr(pts), 0, n, float(p.exaggeration),
-         None, ptr(out.attr), stream())
+    dt = (torch.float64 if torch.float64 in (pts.dtype, p.base_values.dtype)
+          else torch.float32)
+    _check_out(out, dt, "attractive")
+    pts = pts.to(dt)
+    vals = p.base_values.to(dt)
+    call(_lib.fn("bh_attractive", dt), ptr(p.row_offsets),
+         ptr(p.col_indices), ptr(vals), n, 0, ptr(pts), 0, n,
+         float(p.exaggeration), None, ptr(out.attr), stream())
 
 
 def repulsive_bh(t: MortonQuadtree, y, theta: float,
@@ -67,15 +86,17 @@ def repulsive_bh(t: MortonQuadtree, y, theta: float,
         raise ValueError("tree must be summarized before computing repulsion")
     if theta < 0:
         raise ValueError(f"theta must be >= 0, got {theta}")
-    pts = as_points(y)
+    dt = t.arrays.dtype
+    pts = as_points(y, dt)
     n = pts.shape[0]
     if n != t.n_points:
         raise ValueError(f"tree is over {t.n_points} points, embedding has {n}")
+    _check_out(out, dt, "repulsive_bh")
     lib = _lib.load()
     ws = _lib.workspace(lib.bh_repulsive_workspace_bytes(n))
-    call("bh_repulsive", t.arrays.sref(), ptr(t.bounds), float(theta),
-         ptr(pts), 0, n, 0, ptr(out.rep), ptr(out.z_partial), None,
-         ptr(out.z_dev), None, ptr(ws), ws.numel(), stream())
+    call(_lib.fn("bh_repulsive", dt), t.arrays.sref(), ptr(t.bounds),
+         float(theta), ptr(pts), 0, n, 0, ptr(out.rep), ptr(out.z_partial),
+         None, ptr(out.z_dev), None, ptr(ws), ws.numel(), stream())
 
 
 def repulsive_counts(t: MortonQuadtree, theta: float) -> np.ndarray:
@@ -84,12 +105,13 @@ def repulsive_counts(t: MortonQuadtree, theta: float) -> np.ndarray:
     n = t.n_points
     lib = _lib.load()
     dev = t.arrays.node.device
-    rep = torch.empty((n, 2), dtype=torch.float32, device=dev)
+    dt = t.arrays.dtype
+    rep = torch.empty((n, 2), dtype=dt, device=dev)
     cnt = torch.zeros((n, 4), dtype=torch.int32, device=dev)
     ws = _lib.workspace(lib.bh_repulsive_workspace_bytes(n))
-    call("bh_repulsive", t.arrays.sref(), ptr(t.bounds), float(theta), None,
-         0, n, 0, ptr(rep), None, None, None, ptr(cnt), ptr(ws), ws.numel(),
-         stream())
+    call(_lib.fn("bh_repulsive", dt), t.arrays.sref(), ptr(t.bounds),
+         float(theta), None, 0, n, 0, ptr(rep), None, None, None, ptr(cnt),
+         ptr(ws), ws.numel(), stream())
     return cnt.cpu().numpy()
 
 
@@ -99,7 +121,8 @@ def repulsive_exact(y, out: GradientBuffers) -> None:
     n = pts.shape[0]
     if n < 2:
         raise ValueError("need at least 2 points")
+    _check_out(out, pts.dtype, "repulsive_exact")
     lib = _lib.load()
     ws = _lib.workspace(lib.bh_repulsive_exact_workspace_bytes(n))
-    call("bh_repulsive_exact", ptr(pts), n, ptr(out.rep), ptr(out.z_partial),
-         ptr(out.z_dev), ptr(ws), ws.numel(), stream())
+    call(_lib.fn("bh_repulsive_exact", pts.dtype), ptr(pts), n, ptr(out.rep),
+         ptr(out.z_partial), ptr(out.z_dev), ptr(ws), ws.numel(), stream())

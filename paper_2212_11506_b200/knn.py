@@ -16,13 +16,17 @@ from .affinity import NeighborGraph
 
 
 def knn_exact(x, k: int) -> NeighborGraph:
-    data = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)
+    """k exact neighbours; float64 data keeps float64 distances (knn.py:72),
+    anything else runs in float32."""
+    data = torch.as_tensor(np.ascontiguousarray(x)
                            if not isinstance(x, torch.Tensor) else x)
-    data = data.to(_lib.device(), torch.float32).contiguous()
+    dt = torch.float64 if data.dtype == torch.float64 else torch.float32
+    data = data.to(_lib.device(), dt).contiguous()
     n, d = data.shape
     if not 1 <= k <= n - 1:
         raise ValueError(f"k must be in [1, {n - 1}], got {k}")
     idx = torch.empty((n, k), dtype=torch.int64, device=data.device)
-    sqd = torch.empty((n, k), dtype=torch.float32, device=data.device)
-    call("bh_knn", ptr(data), n, d, k, ptr(idx), ptr(sqd), stream())
+    sqd = torch.empty((n, k), dtype=dt, device=data.device)
+    call(_lib.fn("bh_knn", dt), ptr(data), n, d, k, ptr(idx), ptr(sqd),
+         stream())
     return NeighborGraph(idx, sqd)

@@ -6,9 +6,11 @@ Mirrors bhtsne.optimizer (reference: pkg/src/bhtsne/optimizer.py):
 ``kl_divergence`` (:242-270) and ``run`` (:289-332), same defaults, argument
 meaning and error messages.  Differences, all deliberate:
 
-* arrays are CUDA tensors ((N, 2) float32 for y / velocity / gains);
-* ``precision`` is "f32" only (the north-star path computes in float32 with
-  float64 accumulation);
+* arrays are CUDA tensors ((N, 2) y / velocity / gains);
+* ``precision`` defaults to "f32" (the north-star path: float32 storage and
+  pair terms, float64 accumulation); "f64" is the reference's own default
+  mode -- float64 storage and float64 pair terms in the reference's
+  operation order (the library's ``_f64`` kernels);
 * ``run`` takes the kNN graph (``knn=``) computed once by the reference, as
   the north star specifies, or computes it with the exact GPU kNN;
 * ``code_bits`` selects 32-bit Morton codes (default) or the reference's
@@ -25,7 +27,7 @@ from __future__ import annotations
 
 import math
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
@@ -43,7 +45,7 @@ STAGES = ("knn", "bsp", "tree", "summarize", "attractive", "repulsive",
 # "forces": the fused attractive + repulsive launch (Engine.fuse_timed)
 EXTRA_STAGES = ("comm", "relabel", "forces")
 MOMENTUM_SWITCH_ITER = 250
-PRECISIONS = ("f32",)
+PRECISIONS = ("f32", "f64")
 
 
 @dataclass
@@ -85,7 +87,7 @@ class TsneConfig:
         if self.precision not in PRECISIONS:
             raise ValueError(
                 f"unknown precision {self.precision!r}; expected one of "
-                f"{list(PRECISIONS)} (the B200 path is float32)")
+                f"{list(PRECISIONS)}")
         if self.threads is not None and self.threads < 1:
             raise ValueError(f"threads must be >= 1, got {self.threads}")
         if self.code_bits not in (32, 64):
@@ -98,14 +100,14 @@ class TsneConfig:
 
     @property
     def dtype(self):
-        return np.dtype(np.float32)
+        return np.dtype(np.float64 if self.precision == "f64" else np.float32)
 
 
 @dataclass
 class Embedding:
     """(N, 2) points plus optimizer state, resident on the device."""
 
-    y: torch.Tensor   # (N, 2) float32
+    y: torch.Tensor   # (N, 2) float32 | float64 (the run precision)
     v: torch.Tensor   # velocity
     g: torch.Tensor   # adaptive gains (start at 1)
     iteration: int = 0
@@ -168,21 +170,25 @@ def init_embedding(n: int, seed: int, dtype=np.float32) -> Embedding:
     generated on the host (bit-identical Y0) and uploaded once."""
     if n < 2:
         raise ValueError(f"need at least 2 points, got {n}")
-    if np.dtype(dtype) != np.float32:
-        raise ValueError("the B200 path is float32")
+    dt = _lib.torch_dtype(dtype)
     rng = np.random.Generator(np.random.Philox(seed))
-    y = (rng.standard_normal((n, 2)) * 1e-4).astype(np.float32)
+    y = (rng.standard_normal((n, 2)) * 1e-4).astype(
+        np.float64 if dt == torch.float64 else np.float32)
     dev = _lib.device()
     yt = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
     return Embedding(y=yt, v=torch.zeros_like(yt), g=torch.ones_like(yt),
                      iteration=0, rng_seed=int(seed))
 
 
-def embedding_from(y, v=None, g=None, iteration=0) -> Embedding:
-    pts = as_points(y).clone()
+def embedding_from(y, v=None, g=None, iteration=0, dtype=None) -> Embedding:
+    """Embedding from host/device arrays; float64 input (or dtype) keeps the
+    f64 run precision, anything else is float32."""
+    pts = as_points(y, dtype).clone()
     return Embedding(y=pts,
-                     v=torch.zeros_like(pts) if v is None else as_points(v).clone(),
-                     g=torch.ones_like(pts) if g is None else as_points(g).clone(),
+                     v=torch.zeros_like(pts) if v is None
+                     else as_points(v, pts.dtype).clone(),
+                     g=torch.ones_like(pts) if g is None
+                     else as_points(g, pts.dtype).clone(),
                      iteration=iteration)
 
 # ---------------------------------------------------------------------------
@@ -213,7 +219,11 @@ class Engine:
 
     def _fused(self, timed: bool) -> bool:
         return (self.shard is None and self.fuse and not self.overlap
-                and (not timed or self.fuse_timed))
+                and not self.f64 and (not timed or self.fuse_timed))
+
+    def fn(self, name: str) -> str:
+        """Library entry point in the run precision."""
+        return name + "_f64" if self.f64 else name
 
     def _stage_events(self):
         if self.shard is not None:
@@ -232,13 +242,21 @@ class Engine:
         self.code_bits = cfg.code_bits
         dev = e.y.device
         self.dev = dev
-        f2 = lambda: torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        dt = _lib.torch_dtype(cfg.precision)
+        if e.y.dtype != dt:
+            raise ValueError(f"embedding is {e.y.dtype} but precision is "
+                             f"{cfg.precision!r}")
+        self.dtype = dt
+        self.f64 = dt == torch.float64
+        self.pt_bytes = 16 if self.f64 else 8  # one (N, 2) row
+        f2 = lambda: torch.zeros((n, 2), dtype=dt, device=dev)
         i32 = lambda: torch.zeros(n, dtype=torch.int32, device=dev)
         # storage-order state (ids[s] = point id stored at slot s)
         self.y, self.v, self.g, self.tmp = f2(), f2(), f2(), f2()
         self.ids = torch.arange(n, dtype=torch.int32, device=dev)
         self.ids_tmp, self.rank = i32(), i32()
-        self.csr = {"p": p.padded()}
+        rp, col, val = p.padded()
+        self.csr = {"p": (rp, col, val.to(dt))}
         self.csr_key = "p"
         self.attr, self.rep = f2(), f2()
         exag_on = schedule and cfg.n_iter > 0 and cfg.exaggeration_iters > 0
@@ -250,12 +268,16 @@ class Engine:
             momentum_early=cfg.momentum_early,
             momentum_late=cfg.momentum_late,
             learning_rate=cfg.learning_rate, min_gain=cfg.min_gain,
-            bad=INT64_MAX, z=0.0))
+            bad=INT64_MAX, z=0.0,
+            exaggeration_f64=cfg.early_exaggeration,
+            momentum_early_f64=cfg.momentum_early,
+            momentum_late_f64=cfg.momentum_late,
+            learning_rate_f64=cfg.learning_rate, min_gain_f64=cfg.min_gain))
         self.bounds = _lib.struct_tensor(BOUNDS_DTYPE)
         self.codes = torch.zeros(
             n, dtype=torch.int32 if self.code_bits == 32 else torch.int64,
             device=dev)
-        self.tree = TreeArrays(n, self.code_bits, dev)
+        self.tree = TreeArrays(n, self.code_bits, dev, dtype=dt)
         self.ws_sort = _lib.workspace(lib.bh_sort_workspace_bytes(n, self.code_bits))
         self.ws_rep = _lib.workspace(lib.bh_repulsive_workspace_bytes(n))
         self.ws_upd = _lib.workspace(lib.bh_update_workspace_bytes(n))
@@ -322,7 +344,8 @@ class Engine:
         y = self.y
         rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
         rec(0)
-        call("bh_morton", ptr(y), n, ptr(self.bounds), cb, 1, ptr(self.codes), st)
+        call(self.fn("bh_morton"), ptr(y), n, ptr(self.bounds), cb, 1,
+             ptr(self.codes), st)
         if self.shard is None and self.overlap:
             # fork: the memory-bound CSR sweep needs only the centred Y, so
             # it runs on a side stream under the latency-bound sort / tree /
@@ -332,9 +355,9 @@ class Engine:
             with torch.cuda.stream(self.side):
                 self.side.wait_event(self.fork_ev)
                 rec(7)
-                call("bh_attractive", ptr(self.rp), ptr(self.col), ptr(self.val),
-                     n, 1, ptr(y), 0, n, 1.0, ptr(self.sched), ptr(self.attr),
-                     stream())
+                call(self.fn("bh_attractive"), ptr(self.rp), ptr(self.col),
+                     ptr(self.val), n, 1, ptr(y), 0, n, 1.0, ptr(self.sched),
+                     ptr(self.attr), stream())
                 rec(3)
                 self.join_ev.record(self.side)
         call("bh_sort", ptr(self.codes), n, cb, ptr(t.sorted_codes),
@@ -357,12 +380,14 @@ class Engine:
         elif self.shard is None:
             if not self.overlap:  # isolated kernels (stage breakdown)
                 rec(7)
-                call("bh_attractive", ptr(self.rp), ptr(self.col), ptr(self.val),
-                     n, 1, ptr(y), 0, n, 1.0, ptr(self.sched), ptr(self.attr), st)
+                call(self.fn("bh_attractive"), ptr(self.rp), ptr(self.col),
+                     ptr(self.val), n, 1, ptr(y), 0, n, 1.0, ptr(self.sched),
+                     ptr(self.attr), st)
                 rec(3)
-            call("bh_repulsive", t.sref(), ptr(self.bounds), self.theta, None,
-                 0, n, 0, ptr(self.rep), None, None, ptr(self.z_dev), None,
-                 ptr(self.ws_rep), self.ws_rep.numel(), st)
+            call(self.fn("bh_repulsive"), t.sref(), ptr(self.bounds),
+                 self.theta, None, 0, n, 0, ptr(self.rep), None, None,
+                 ptr(self.z_dev), None, ptr(self.ws_rep), self.ws_rep.numel(),
+                 st)
             rec(4)
             if self.overlap:
                 torch.cuda.current_stream().wait_event(self.join_ev)
@@ -370,9 +395,9 @@ class Engine:
             rep, rep_rank = self.rep, None
         else:
             rep, rep_rank = self.shard.forces(self, rec, st)
-        call("bh_update", ptr(y), ptr(self.v), ptr(self.g), ptr(self.attr),
-             ptr(rep), ptr(rep_rank), n, ptr(self.sched), ptr(self.bounds), cb,
-             ptr(self.ws_upd), self.ws_upd.numel(), st)
+        call(self.fn("bh_update"), ptr(y), ptr(self.v), ptr(self.g),
+             ptr(self.attr), ptr(rep), ptr(rep_rank), n, ptr(self.sched),
+             ptr(self.bounds), cb, ptr(self.ws_upd), self.ws_upd.numel(), st)
         rec(6)
 
     def _events(self, k):
@@ -428,8 +453,9 @@ class Engine:
         torch.cuda.synchronize()
 
     # -- storage order -----------------------------------------------------
-    def _rows(self, name, src, idx, dst, nbytes=8):
-        call(name, ptr(src), ptr(idx), self.n, nbytes, ptr(dst), stream())
+    def _rows(self, name, src, idx, dst, nbytes=None):
+        call(name, ptr(src), ptr(idx), self.n, nbytes or self.pt_bytes,
+             ptr(dst), stream())
 
     def load(self):
         """Point-id order (Embedding) -> storage order."""
@@ -457,21 +483,22 @@ class Engine:
         self._alloc_relabel()
         rp, col, val = self.csr[self.csr_key]
         orp, ocol, oval = self.csr[nxt]
-        call("bh_permute_csr", ptr(rp), ptr(col), ptr(val), ptr(order),
-             ptr(self.rank), self.n, ptr(orp), ptr(ocol), ptr(oval),
-             ptr(self.ws_perm), self.ws_perm.numel(), st)
+        call(self.fn("bh_permute_csr"), ptr(rp), ptr(col), ptr(val),
+             ptr(order), ptr(self.rank), self.n, ptr(orp), ptr(ocol),
+             ptr(oval), ptr(self.ws_perm), self.ws_perm.numel(), st)
         self.csr_key = nxt
         self.since_relabel = 0
 
     # -- driver --------------------------------------------------------------
     def begin(self):
         """Bounds of the current (centred) Y, shift 0."""
-        call("bh_bounds", ptr(self.y), self.n, self.code_bits,
+        call(self.fn("bh_bounds"), ptr(self.y), self.n, self.code_bits,
              ptr(self.bounds), ptr(self.ws_bnd), self.ws_bnd.numel(), stream())
 
     def end(self):
         """Apply the pending re-centering of the last update."""
-        call("bh_center", ptr(self.y), self.n, ptr(self.bounds), stream())
+        call(self.fn("bh_center"), ptr(self.y), self.n, ptr(self.bounds),
+             stream())
 
     def set_iteration(self, it: int, exaggeration: float | None = None):
         """Host override of the schedule (stage API: p carries the factor)."""
@@ -479,6 +506,7 @@ class Engine:
         host["iteration"] = it
         if exaggeration is not None:
             host["exaggeration"] = np.float32(exaggeration)
+            host["exaggeration_f64"] = float(exaggeration)
             host["exaggeration_iters"] = np.iinfo(np.int32).max
         self.sched.copy_(torch.from_numpy(
             np.array([host], SCHED_DTYPE).view(np.uint8)).to(self.dev))
@@ -567,9 +595,14 @@ def gradient_step(e: Embedding, p: SparseAffinity, cfg: TsneConfig,
     cfg.validate()
     eng = getattr(e, "_engine", None)
     if (eng is None or eng.p.base_values is not p.base_values
-            or eng.cfg is not cfg):
-        eng = Engine(p, e, cfg, schedule=False)
+            or getattr(e, "_engine_cfg", None) is not cfg):
+        # the embedding's dtype is the run precision, as in the reference
+        # (optimizer.py:200, 214)
+        prec = "f64" if e.y.dtype == torch.float64 else "f32"
+        run_cfg = cfg if cfg.precision == prec else replace(cfg, precision=prec)
+        eng = Engine(p, e, run_cfg, schedule=False)
         e._engine = eng
+        e._engine_cfg = cfg
     eng.set_iteration(e.iteration, exaggeration=p.exaggeration)
     eng.run(1, timings, use_graph=False)
     if buffers is not None:
@@ -590,7 +623,9 @@ def kl_divergence(p: SparseAffinity, y, mode: str = "exact",
     n = pts.shape[0]
     if p.n != n:
         raise ValueError(f"matrix is over {p.n} points, embedding has {n}")
-    buffers = GradientBuffers.allocate(n)
+    if torch.float64 in (pts.dtype, p.dtype):  # mixed inputs: promote
+        pts = pts.to(torch.float64)
+    buffers = GradientBuffers.allocate(n, pts.dtype)
     if mode == "exact":
         repulsive_exact(pts, buffers)
     elif mode == "bh":
@@ -603,9 +638,10 @@ def kl_divergence(p: SparseAffinity, y, mode: str = "exact",
     lib = _lib.load()
     out = torch.zeros(1, dtype=torch.float64, device=pts.device)
     ws = _lib.workspace(lib.bh_kl_workspace_bytes(n))
-    call("bh_kl_rows", ptr(p.row_offsets), ptr(p.col_indices),
-         ptr(p.base_values), n, 0, ptr(pts), ptr(buffers.z_dev), ptr(out),
-         ptr(ws), ws.numel(), stream())
+    vals = p.base_values.to(pts.dtype)
+    call(_lib.fn("bh_kl_rows", pts.dtype), ptr(p.row_offsets),
+         ptr(p.col_indices), ptr(vals), n, 0, ptr(pts), ptr(buffers.z_dev),
+         ptr(out), ptr(ws), ws.numel(), stream())
     return float(out.item())
 
 
@@ -614,7 +650,7 @@ def affinities(x, cfg: TsneConfig, knn=None, timings=None):
     tick = time.perf_counter
     if knn is None:
         from .knn import knn_exact
-        data = np.ascontiguousarray(getattr(x, "data", x), dtype=np.float32)
+        data = np.ascontiguousarray(getattr(x, "data", x), dtype=cfg.dtype)
         n = data.shape[0]
         k = min(int(math.floor(3 * cfg.perplexity)), n - 1)
         t0 = tick()
@@ -627,7 +663,7 @@ def affinities(x, cfg: TsneConfig, knn=None, timings=None):
     graph = as_graph(knn)
     t0 = tick()
     pr = calibrate_perplexity(graph, cfg.perplexity)
-    p = symmetrize(pr, graph)
+    p = symmetrize(pr, graph, dtype=cfg.dtype)
     torch.cuda.synchronize()
     if timings is not None:
         timings.add("bsp", tick() - t0)
@@ -646,7 +682,7 @@ def run(x, cfg: TsneConfig, *, knn=None) -> tuple:
     data = getattr(x, "data", x)
     n = int(np.shape(data)[0]) if knn is None else as_graph(knn).n_points
     p, _ = affinities(x, cfg, knn=knn, timings=timings)
-    e = init_embedding(n, cfg.seed)
+    e = init_embedding(n, cfg.seed, dtype=cfg.dtype)
     eng = Engine(p, e, cfg, schedule=True)
     kl_history = []
     done = 0

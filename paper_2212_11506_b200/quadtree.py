@@ -9,6 +9,11 @@ Code width: ``code_bits=32`` (default, 16 bits per dimension, depth <= 16,
 the north-star layout) or ``64`` (the reference's own width, depth <= 32).
 ``MortonQuadtree.to_reference()`` returns the reference array layout
 (quadtree.py:66-85) for parity checks.
+
+Precision follows the points, as in the reference (whose kernels run on the
+arrays' own dtype): float64 points build an f64 tree (f64 centres of mass,
+32-byte records) and select the library's ``_f64`` entry points; anything
+else runs in float32.
 """
 
 from __future__ import annotations
@@ -25,9 +30,10 @@ from ._lib import BOUNDS_DTYPE, call, ptr, stream
 DEFAULT_CODE_BITS = 32
 
 
-def as_points(y) -> torch.Tensor:
-    """(N, 2) or (y0, y1) -> contiguous (N, 2) float32 CUDA tensor
-    (quadtree.py:122-130 accepts both forms)."""
+def as_points(y, dtype=None) -> torch.Tensor:
+    """(N, 2) or (y0, y1) -> contiguous (N, 2) CUDA tensor (quadtree.py:
+    122-130 accepts both forms), float64 if the input is float64 (or
+    ``dtype`` asks for it), else float32."""
     dev = _lib.device()
     if isinstance(y, tuple):
         y0, y1 = (torch.as_tensor(a) for a in y)
@@ -36,7 +42,9 @@ def as_points(y) -> torch.Tensor:
         t = torch.as_tensor(y)
         if t.ndim != 2 or t.shape[1] != 2:
             raise ValueError(f"expected (N, 2) points, got shape {tuple(t.shape)}")
-    return t.to(device=dev, dtype=torch.float32).contiguous()
+    if dtype is None:
+        dtype = torch.float64 if t.dtype == torch.float64 else torch.float32
+    return t.to(device=dev, dtype=_lib.torch_dtype(dtype)).contiguous()
 
 
 def _bounds_struct(center, r_span, code_bits, shift=(0.0, 0.0)):
@@ -58,8 +66,8 @@ def compute_bounds(y, code_bits: int = DEFAULT_CODE_BITS):
     lib = _lib.load()
     out = _lib.struct_tensor(BOUNDS_DTYPE)
     ws = _lib.workspace(lib.bh_bounds_workspace_bytes(n))
-    call("bh_bounds", ptr(pts), n, code_bits, ptr(out), ptr(ws), ws.numel(),
-         stream())
+    call(_lib.fn("bh_bounds", pts.dtype), ptr(pts), n, code_bits, ptr(out),
+         ptr(ws), ws.numel(), stream())
     b = _lib.read_struct(out, BOUNDS_DTYPE)
     if b["nonfinite"]:
         raise ValueError("non-finite coordinate in embedding points")
@@ -110,7 +118,8 @@ def morton_codes(y, center, r_span: float,
     sorted_codes = torch.empty_like(codes)
     order = torch.empty(n, dtype=torch.int32, device=pts.device)
     b = _bounds_struct(center, r_span, code_bits)
-    call("bh_morton", ptr(pts), n, ptr(b), code_bits, 0, ptr(codes), stream())
+    call(_lib.fn("bh_morton", pts.dtype), ptr(pts), n, ptr(b), code_bits, 0,
+         ptr(codes), stream())
     ws = _lib.workspace(lib.bh_sort_workspace_bytes(n, code_bits))
     call("bh_sort", ptr(codes), n, code_bits, ptr(sorted_codes), ptr(order),
          ptr(ws), ws.numel(), stream())
@@ -123,15 +132,19 @@ def morton_codes(y, center, r_span: float,
 class TreeArrays:
     """Device storage of one bh_tree_t (caller-owned, reusable)."""
 
-    def __init__(self, n: int, code_bits: int, device, capacity=None):
+    def __init__(self, n: int, code_bits: int, device, capacity=None,
+                 dtype=torch.float32):
         lib = _lib.load()
         self.n = n
         self.code_bits = code_bits
         self.max_depth = code_bits // 2
+        self.dtype = _lib.torch_dtype(dtype)
+        self.precision = 64 if self.dtype == torch.float64 else 32
         cap = int(capacity or lib.bh_tree_node_bound(n, code_bits))
         self.capacity = cap
         i32 = dict(dtype=torch.int32, device=device)
-        self.node = torch.zeros((cap, 4), dtype=torch.float32, device=device)
+        # records: 4 x f32 (16 B) or 4 x f64 (32 B: com, then mass|info)
+        self.node = torch.zeros((cap, 4), dtype=self.dtype, device=device)
         self.parent = torch.zeros(cap, **i32)
         self.node_start = torch.zeros(cap, **i32)
         self.leaf_end = torch.zeros(cap, **i32)
@@ -140,7 +153,7 @@ class TreeArrays:
         self.sorted_codes = torch.zeros(
             n, dtype=torch.int32 if code_bits == 32 else torch.int64,
             device=device)
-        self.ys = torch.zeros((n, 2), dtype=torch.float32, device=device)
+        self.ys = torch.zeros((n, 2), dtype=self.dtype, device=device)
         self.status = torch.zeros(1, **i32)
         self.ws = _lib.workspace(lib.bh_tree_workspace_bytes(n, code_bits))
         self.struct = _lib.TreeStruct(
@@ -152,7 +165,7 @@ class TreeArrays:
             level_off=self.level_off.data_ptr(),
             order=self.order.data_ptr(),
             sorted_codes=self.sorted_codes.data_ptr(), ys=self.ys.data_ptr(),
-            status=self.status.data_ptr())
+            status=self.status.data_ptr(), precision=self.precision)
 
     def sref(self):
         return C.byref(self.struct)
@@ -217,8 +230,12 @@ class MortonQuadtree:
         lo = self.level_offsets
         m = int(lo[-1])
         rec = self.arrays.node[:m].cpu().numpy()
-        info = rec[:, 3].view(np.uint32).astype(np.int64)
-        mass = rec[:, 2].view(np.uint32).astype(np.int64)
+        if self.arrays.precision == 64:
+            mi = np.ascontiguousarray(rec[:, 2]).view(np.uint32).reshape(m, 2)
+            mass, info = (mi[:, 0].astype(np.int64), mi[:, 1].astype(np.int64))
+        else:
+            info = rec[:, 3].view(np.uint32).astype(np.int64)
+            mass = rec[:, 2].view(np.uint32).astype(np.int64)
         is_leaf = ((info & _lib.BH_LEAF_BIT) != 0).astype(np.uint8)
         start = self.arrays.node_start[:m].cpu().numpy().astype(np.int64)
         parent = self.arrays.parent[:m].cpu().numpy().astype(np.int64)
@@ -250,7 +267,7 @@ class MortonQuadtree:
                    is_leaf=is_leaf, cell_center=center, cell_radius=radius,
                    mass=mass if self.summarized else np.zeros(m, np.int64),
                    com=rec[:, :2].copy() if self.summarized
-                   else np.zeros((m, 2), np.float32),
+                   else np.zeros((m, 2), rec.dtype),
                    order=self.order.cpu().numpy().astype(np.int64),
                    ys0=ys[:, 0].copy(), ys1=ys[:, 1].copy(), depth=depth,
                    sorted_codes=sc)
@@ -277,7 +294,8 @@ class MortonQuadtree:
 def build_tree(mc: MortonCodes, y, capacity=None) -> MortonQuadtree:
     """Build the canonical quadtree over the sorted codes (quadtree.py:399)."""
     pts = as_points(y)
-    arrays = TreeArrays(pts.shape[0], mc.code_bits, pts.device, capacity)
+    arrays = TreeArrays(pts.shape[0], mc.code_bits, pts.device, capacity,
+                        dtype=pts.dtype)
     arrays.order.copy_(mc.order)
     arrays.sorted_codes.copy_(mc.sorted_codes)
     arrays.build(pts)

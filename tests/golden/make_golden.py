@@ -56,6 +56,23 @@ TREE_FIELDS = ("level_offsets", "start", "end", "children", "is_leaf",
                "ys1")
 
 
+def point_sets_f64():
+    """float64 point sets (the reference's default run precision): values
+    that are not float32-representable, plus exact duplicates."""
+    sets = {}
+    rng = np.random.default_rng(21)
+    sets["gauss2000"] = rng.standard_normal((2000, 2))
+    rng = np.random.default_rng(22)
+    core = rng.standard_normal((1200, 2)) * 1e-4
+    tails = rng.standard_t(2.0, (1200, 2)) * 5.0
+    dup = np.repeat(rng.standard_normal((15, 2)), 20, axis=0)
+    y = np.vstack([core, tails, dup])
+    sets["heavy2700"] = y[rng.permutation(y.shape[0])]
+    sets["coinc7"] = np.array([[1.0, 1.0]] * 5 + [[-1.0, -1.0]] * 2) + 1e-12
+    sets["two"] = np.array([[0.0, 0.0], [0.1, 3.0]])
+    return sets
+
+
 def _tree_case(bhtsne, y, mode):
     from bhtsne import quadtree as q
     center, r_span = bhtsne.compute_bounds(y)
@@ -73,12 +90,12 @@ def _tree_case(bhtsne, y, mode):
         out[f] = getattr(t, f)
     if y.shape[0] >= 2:
         for theta in (0.0, 0.5, 0.8):
-            b = bhtsne.GradientBuffers.allocate(y.shape[0], np.float32)
+            b = bhtsne.GradientBuffers.allocate(y.shape[0], y.dtype)
             bhtsne.repulsive_bh(t, y, theta, b)
             tag = f"bh{int(theta * 10)}"
             out[tag + "_rep0"], out[tag + "_rep1"] = b.rep0, b.rep1
             out[tag + "_zpart"], out[tag + "_z"] = b.z_partial, np.array(b.z)
-        b = bhtsne.GradientBuffers.allocate(y.shape[0], np.float32)
+        b = bhtsne.GradientBuffers.allocate(y.shape[0], y.dtype)
         bhtsne.repulsive_exact(y, b)
         out["ex_rep0"], out["ex_rep1"] = b.rep0, b.rep1
         out["ex_zpart"], out["ex_z"] = b.z_partial, np.array(b.z)
@@ -97,6 +114,13 @@ def child_trees(mode: int):
         np.savez_compressed(os.path.join(HERE, f"tree{mode}_{name}.npz"),
                             **out)
         print(f"tree{mode}_{name}: nodes={out['start'].shape[0]}", flush=True)
+    # the f64 run precision: f64 centres of mass and f64 pair terms
+    for name, y in point_sets_f64().items():
+        out = _tree_case(bhtsne, y, mode)
+        np.savez_compressed(os.path.join(HERE, f"tree{mode}f64_{name}.npz"),
+                            **out)
+        print(f"tree{mode}f64_{name}: nodes={out['start'].shape[0]}",
+              flush=True)
 
 
 def affinity_and_forces():
@@ -153,6 +177,46 @@ def affinity_and_forces():
                         attr_two=b2.attr)
 
 
+def affinity_f64():
+    """The affinity / attractive / KL / trajectory fixtures of
+    affinity_and_forces() in the reference's f64 run precision."""
+    import bhtsne
+    rng = np.random.default_rng(24)
+    centres = rng.uniform(-5, 5, (3, 8))
+    x = centres[np.repeat(np.arange(3), 150)] + rng.standard_normal((450, 8))
+    g = bhtsne.knn_exact(bhtsne.InputMatrix(x), 30)
+    pr = bhtsne.calibrate_perplexity(g, 10.0)
+    p = bhtsne.symmetrize(pr, g, dtype=np.float64)
+    y = rng.standard_normal((450, 2)) * 3
+    buf = bhtsne.GradientBuffers.allocate(450, np.float64)
+    bhtsne.attractive(p, y, buf)
+    p12 = bhtsne.set_exaggeration(p, 12.0)
+    buf12 = bhtsne.GradientBuffers.allocate(450, np.float64)
+    bhtsne.attractive(p12, y, buf12)
+    kl = bhtsne.kl_divergence(p, y)
+    kl_bh = bhtsne.kl_divergence(p, y, mode="bh", theta=0.5)
+    out = dict(x=x, indices=g.indices, sq_distances=g.sq_distances,
+               betas=pr.betas, cond=pr.conditional, row_offsets=p.row_offsets,
+               col_indices=p.col_indices, values=p.values, y=y,
+               attr0=buf.attr0, attr1=buf.attr1, attr12_0=buf12.attr0,
+               attr12_1=buf12.attr1, kl=np.array(kl), kl_bh=np.array(kl_bh))
+    cfg = bhtsne.TsneConfig(precision="f64", perplexity=10.0)
+    e = bhtsne.init_embedding(450, seed=3, dtype=np.float64)
+    out["y0_init"], out["y1_init"] = e.y0.copy(), e.y1.copy()
+    pe = bhtsne.set_exaggeration(p, 12.0)
+    for it in range(8):
+        buffers = bhtsne.GradientBuffers.allocate(450, np.float64)
+        pp = pe if it < 4 else p
+        if it == 4:  # jump over the momentum switch to exercise both branches
+            e.iteration = 250
+        bhtsne.gradient_step(e, pp, cfg, buffers=buffers)
+        out[f"y0_{it}"], out[f"y1_{it}"] = e.y0.copy(), e.y1.copy()
+        out[f"v0_{it}"], out[f"g0_{it}"] = e.v0.copy(), e.g0.copy()
+        out[f"z_{it}"] = np.array(buffers.z)
+    np.savez_compressed(os.path.join(HERE, "affinity450f64.npz"), **out)
+    print("affinity450f64 nnz", p.nnz, "kl", kl, "kl_bh", kl_bh)
+
+
 def full_run_c0():
     """C0 (BASELINE.json configs[0]) full 1000-iteration f32 run."""
     import bhtsne
@@ -179,10 +243,13 @@ def main():
             child_trees(32)
         elif what == "affinity":
             affinity_and_forces()
+        elif what == "affinity_f64":
+            affinity_f64()
         elif what == "c0":
             full_run_c0()
         return
-    jobs = sys.argv[1:] or ["trees64", "trees32", "affinity", "c0"]
+    jobs = sys.argv[1:] or ["trees64", "trees32", "affinity", "affinity_f64",
+                            "c0"]
     for what in jobs:
         with tempfile.TemporaryDirectory() as cache:
             env = dict(os.environ, PYTHONPATH=REF_SRC, NUMBA_CACHE_DIR=cache)
