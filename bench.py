@@ -295,7 +295,8 @@ def ours_arm(args, rank, world):
                     y0=prob["y0"].astype(np.float64))
     p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
     cfg = bh.TsneConfig(theta=args.theta, graph_chunk=args.chunk,
-                        precision=args.precision)
+                        precision=args.precision,
+                        relabel_every=args.relabel_every)
     e = bh.embedding_from(prob["y0"])
     shard = None
     if world > 1:
@@ -304,6 +305,7 @@ def ours_arm(args, rank, world):
     eng = bh.Engine(p, e, cfg, schedule=True, shard=shard)
     eng.overlap = args.overlap
     eng.fuse = not args.no_fuse
+    eng.chunk_graph = not args.no_chunk_graph
     eng.prepare(timings=True)  # every CUDA graph captured before timing
     if args.preroll:
         eng.run(args.preroll)
@@ -641,6 +643,10 @@ def main():
     ap.add_argument("--e2e-repeats", type=int, default=3,
                     help="end-to-end runs through the public API (median)")
     ap.add_argument("--ref-max-steps", type=int, default=3)
+    ap.add_argument("--relabel-every", type=int, default=50,
+                    help="Morton relabeling period of the engine (0: never)")
+    ap.add_argument("--no-chunk-graph", action="store_true",
+                    help="replay a one-iteration graph per step (A/B)")
     ap.add_argument("--no-fuse", action="store_true",
                     help="separate attractive/repulsive launches in the "
                          "timed region (A/B of the fused force pass)")

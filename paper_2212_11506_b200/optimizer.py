@@ -304,6 +304,8 @@ class Engine:
         self.fuse = True
         self.fuse_timed = False
         self.launches = 0  # library kernels enqueued by run() (bench claim)
+        # full chunks of the fast path replay one graph_chunk-iteration graph
+        self.chunk_graph = True
         self.fork_ev = torch.cuda.Event()
         self.join_ev = torch.cuda.Event()
         self.shard = shard
@@ -427,6 +429,19 @@ class Engine:
             self.graphs[key] = g
         return self.graphs[key]
 
+    def _graphk(self):
+        """graph_chunk iterations in one graph without timing events: one
+        graph launch per chunk instead of one per iteration."""
+        k = self.cfg.graph_chunk
+        key = ("fastk", k, self.csr_key, self.overlap, self._fused(False))
+        if key not in self.graphs:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.main):
+                for _ in range(k):
+                    self._enqueue(None)
+            self.graphs[key] = g
+        return self.graphs[key]
+
     def _alloc_relabel(self):
         if "A" not in self.csr:
             rp, col, val = self.csr["p"]
@@ -447,6 +462,8 @@ class Engine:
             for key in keys:
                 self.csr_key = key
                 self._graph1()
+                if self.chunk_graph:
+                    self._graphk()
                 if timings:
                     self._graph(self.cfg.graph_chunk)
         self.csr_key = cur
@@ -545,9 +562,12 @@ class Engine:
             k = min(chunk, n_iter - done)
             evs = None
             if use_graph and timings is None:
-                g = self._graph1()
-                for _ in range(k):
-                    g.replay()
+                if self.chunk_graph and k == self.cfg.graph_chunk:
+                    self._graphk().replay()
+                else:
+                    g = self._graph1()
+                    for _ in range(k):
+                        g.replay()
             elif use_graph:
                 g, evs = self._graph(k)
                 g.replay()
