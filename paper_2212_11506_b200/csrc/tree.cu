@@ -21,6 +21,8 @@
 // schedule): a node's children are the consecutive next-level nodes whose
 // parent is the node; f64 sums in the reference's child order, so centres
 // of mass are bit-identical to the reference's.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bh {
@@ -199,18 +201,12 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
 // mass = sum, com = sum(m_ch * f64(com_ch)) / m in child order.  Leaves
 // still open here are depth-D buckets: f64 mean of their points in order.
 template <typename T>
-__global__ void __launch_bounds__(kSumThreads)
-k_summarize_level(void *__restrict__ node, const int32_t *__restrict__ parent,
-                  const int32_t *__restrict__ leaf_end,
-                  const p2_t<T> *__restrict__ ys,
-                  const int32_t *__restrict__ level_off, int d, int D,
-                  const int32_t *__restrict__ status) {
+__device__ __forceinline__ void summarize_node(
+    void *__restrict__ node, const int32_t *__restrict__ parent,
+    const int32_t *__restrict__ leaf_end, const p2_t<T> *__restrict__ ys,
+    int32_t nd, int d, int D, int32_t hi_next) {
     using Rec = NodeRec<T>;
-    if (*status != BH_OK) return;
-    const int32_t lo = level_off[d], hi = level_off[d + 1];
-    const int32_t hi_next = d < D ? level_off[d + 2] : hi;
-    for (int32_t nd = lo + blockIdx.x * kSumThreads + threadIdx.x; nd < hi;
-         nd += gridDim.x * kSumThreads) {
+    do {
         const uint32_t info = Rec::info(node, nd);
         if (info & BH_LEAF_BIT) {
             if (d < D) continue;  // single-point leaf, completed by emit
@@ -247,6 +243,43 @@ k_summarize_level(void *__restrict__ node, const int32_t *__restrict__ parent,
         Rec::store(node, nd,
                    mk2<T>((T)__ddiv_rn(a, (double)m), (T)__ddiv_rn(b, (double)m)),
                    m, fc | ((k - 1) << BH_NKIDS_SHIFT));
+    } while (false);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSumThreads)
+k_summarize_level(void *__restrict__ node, const int32_t *__restrict__ parent,
+                  const int32_t *__restrict__ leaf_end,
+                  const p2_t<T> *__restrict__ ys,
+                  const int32_t *__restrict__ level_off, int d, int D,
+                  const int32_t *__restrict__ status) {
+    if (*status != BH_OK) return;
+    const int32_t lo = level_off[d], hi = level_off[d + 1];
+    const int32_t hi_next = d < D ? level_off[d + 2] : hi;
+    for (int32_t nd = lo + blockIdx.x * kSumThreads + threadIdx.x; nd < hi;
+         nd += gridDim.x * kSumThreads)
+        summarize_node<T>(node, parent, leaf_end, ys, nd, d, D, hi_next);
+}
+
+// Levels dtop..0 (at most 4^dtop nodes each) in ONE CTA, deepest first with
+// a CTA barrier between levels: the small top of the tree costs one launch
+// instead of dtop + 1.
+constexpr int kSumTopThreads = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(kSumTopThreads)
+k_summarize_top(void *__restrict__ node, const int32_t *__restrict__ parent,
+                const int32_t *__restrict__ leaf_end,
+                const p2_t<T> *__restrict__ ys,
+                const int32_t *__restrict__ level_off, int dtop, int D,
+                const int32_t *__restrict__ status) {
+    if (*status != BH_OK) return;
+    for (int d = dtop; d >= 0; d--) {
+        const int32_t lo = level_off[d], hi = level_off[d + 1];
+        const int32_t hi_next = d < D ? level_off[d + 2] : hi;
+        for (int32_t nd = lo + threadIdx.x; nd < hi; nd += kSumTopThreads)
+            summarize_node<T>(node, parent, leaf_end, ys, nd, d, D, hi_next);
+        __syncthreads();
     }
 }
 
@@ -329,7 +362,12 @@ extern "C" int bh_summarize(const bh_tree_t *t, void *ws, size_t ws_bytes,
     }();
     int grid = bh_blocks(t->n_points, kSumThreads);
     if (grid > max_blocks) grid = max_blocks;
-    for (int d = D; d >= 0; d--) {
+    static const int top = [] {  // tuning knob BH_SUM_TOP (-1: off)
+        const char *s = getenv("BH_SUM_TOP");
+        return s ? atoi(s) : 6;
+    }();
+    const int dtop = std::min(top, D);
+    for (int d = D; d > dtop; d--) {
         if (tree_f64(t))
             k_summarize_level<double><<<grid, kSumThreads, 0, bh_cs(stream)>>>(
                 (void *)t->node, t->parent, t->leaf_end,
@@ -339,6 +377,17 @@ extern "C" int bh_summarize(const bh_tree_t *t, void *ws, size_t ws_bytes,
                 (void *)t->node, t->parent, t->leaf_end, (const float2 *)t->ys,
                 t->level_off, d, D, t->status);
         BH_CHECK_LAUNCH("k_summarize_level");
+    }
+    if (dtop >= 0) {
+        if (tree_f64(t))
+            k_summarize_top<double><<<1, kSumTopThreads, 0, bh_cs(stream)>>>(
+                (void *)t->node, t->parent, t->leaf_end,
+                (const double2 *)t->ys, t->level_off, dtop, D, t->status);
+        else
+            k_summarize_top<float><<<1, kSumTopThreads, 0, bh_cs(stream)>>>(
+                (void *)t->node, t->parent, t->leaf_end, (const float2 *)t->ys,
+                t->level_off, dtop, D, t->status);
+        BH_CHECK_LAUNCH("k_summarize_top");
     }
     return BH_OK;
 }

@@ -26,6 +26,7 @@ CUDA events captured in the graph (exact per-iteration StepTimings).
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field, replace
 
@@ -333,10 +334,14 @@ class Engine:
     def kernels_per_iteration(self, timed: bool = False) -> int:
         """Library kernel launches of one iteration: morton, sort histogram +
         one pass per code byte, 3 tree kernels, one summarize kernel per
-        level (code_bits / 2 + 1), the force pass (1 fused or attractive +
+        level below the top 7 plus one for levels 6..0 (tree.cu), the force
+        pass (1 fused or attractive +
         repulsive), update; + the Z-partials sum when sharded."""
         forces = 1 if self._fused(timed) else 2
-        return (1 + 1 + self.code_bits // 8 + 3 + (self.code_bits // 2 + 1)
+        depth = self.code_bits // 2
+        top = min(int(os.environ.get("BH_SUM_TOP", 6)), depth)  # tree.cu
+        summarize = depth - top + (1 if top >= 0 else 0)
+        return (1 + 1 + self.code_bits // 8 + 3 + summarize
                 + forces + 1 + (1 if self.shard is not None else 0))
 
     # -- one iteration -----------------------------------------------------
