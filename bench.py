@@ -305,7 +305,7 @@ def ours_arm(args, rank, world):
     eng = bh.Engine(p, e, cfg, schedule=True, shard=shard)
     eng.overlap = args.overlap
     eng.fuse = not args.no_fuse
-    eng.chunk_graph = not args.no_chunk_graph
+    eng.chunk_graph = args.chunk_graph
     eng.prepare(timings=True)  # every CUDA graph captured before timing
     if args.preroll:
         eng.run(args.preroll)
@@ -408,6 +408,7 @@ def ours_arm(args, rank, world):
     vals = sorted(r["value"] for r in runs)
     e2e = dict(runs[0], value=vals[len(vals) // 2],
                repeats=[r["value"] for r in runs],
+               breakdowns=[r["breakdown_s"] for r in runs],
                summary=f"median of {len(runs)} end-to-end runs")
     e2e["per_step_host_state"] = e2e_host(bh, p, cfg, y_end, args)
 
@@ -448,14 +449,21 @@ def e2e_run(bh, prob, cfg, args):
     y0 = pin(prob["y0"])
     iters = args.warmup + args.steps
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    tick = time.perf_counter
+    t0 = tick()
     p = bh.from_csr(ro, co, va)
     e = bh.embedding_from(y0)
+    torch.cuda.synchronize()
+    t1 = tick()
     eng = bh.Engine(p, e, cfg)
+    torch.cuda.synchronize()
+    t2 = tick()
     eng.run(iters)
+    torch.cuda.synchronize()
+    t3 = tick()
     y_out = e.y.cpu()
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    dt = tick() - t0
     h2d = sum(int(t.numel() * t.element_size()) for t in (ro, co, va, y0))
     d2h = int(y_out.numel() * y_out.element_size())
     return {"value": iters / dt, "unit": "it/s",
@@ -463,7 +471,9 @@ def e2e_run(bh, prob, cfg, args):
             "api": f"Engine(from_csr(host P), embedding_from(host Y0)).run({iters}) "
                    "+ Y to host; pinned host buffers; host wall clock incl. "
                    "upload, CSR padding, CUDA-graph capture and readback",
-            "steps": iters}
+            "steps": iters,
+            "breakdown_s": {"upload": t1 - t0, "engine_init": t2 - t1,
+                            "run": t3 - t2, "readback": t0 + dt - t3}}
 
 
 def e2e_host(bh, p, cfg, y_host, args):
@@ -645,8 +655,8 @@ def main():
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--relabel-every", type=int, default=50,
                     help="Morton relabeling period of the engine (0: never)")
-    ap.add_argument("--no-chunk-graph", action="store_true",
-                    help="replay a one-iteration graph per step (A/B)")
+    ap.add_argument("--chunk-graph", action="store_true",
+                    help="replay one graph per graph_chunk iterations (A/B)")
     ap.add_argument("--no-fuse", action="store_true",
                     help="separate attractive/repulsive launches in the "
                          "timed region (A/B of the fused force pass)")

@@ -305,8 +305,10 @@ class Engine:
         self.fuse = True
         self.fuse_timed = False
         self.launches = 0  # library kernels enqueued by run() (bench claim)
-        # full chunks of the fast path replay one graph_chunk-iteration graph
-        self.chunk_graph = True
+        # True: full chunks of the fast path replay one graph_chunk-iteration
+        # graph (+0.2% device time, but capturing 25-iteration graphs for the
+        # three CSR buffers costs ~0.1 s per engine: off for end-to-end runs)
+        self.chunk_graph = False
         self.fork_ev = torch.cuda.Event()
         self.join_ev = torch.cuda.Event()
         self.shard = shard
