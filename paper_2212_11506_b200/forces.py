@@ -57,10 +57,19 @@ class GradientBuffers:
     rep1 = property(lambda s: s.rep[:, 1])
 
 
-def _check_out(out: GradientBuffers, dt: torch.dtype, what: str):
-    if out.dtype != dt:
-        raise ValueError(f"{what}: buffers are {out.dtype}, the inputs run in "
-                         f"{dt} (allocate GradientBuffers with that dtype)")
+class _Out:
+    """An (N, 2) result in the run precision ``dt``, stored into ``dst``
+    (cast when the caller's buffers have another dtype, as numpy does when
+    the reference's kernels write f64 results into f32 buffers)."""
+
+    def __init__(self, dst: torch.Tensor, dt: torch.dtype):
+        self.dst = dst
+        self.t = dst if dst.dtype == dt else torch.empty(
+            dst.shape, dtype=dt, device=dst.device)
+
+    def done(self):
+        if self.t is not self.dst:
+            self.dst.copy_(self.t)
 
 
 def attractive(p, y, out: GradientBuffers) -> None:
@@ -71,12 +80,13 @@ def attractive(p, y, out: GradientBuffers) -> None:
         raise ValueError(f"matrix is over {p.n} points, embedding has {n}")
     dt = (torch.float64 if torch.float64 in (pts.dtype, p.base_values.dtype)
           else torch.float32)
-    _check_out(out, dt, "attractive")
+    res = _Out(out.attr, dt)
     pts = pts.to(dt)
     vals = p.base_values.to(dt)
     call(_lib.fn("bh_attractive", dt), ptr(p.row_offsets),
          ptr(p.col_indices), ptr(vals), n, 0, ptr(pts), 0, n,
-         float(p.exaggeration), None, ptr(out.attr), stream())
+         float(p.exaggeration), None, ptr(res.t), stream())
+    res.done()
 
 
 def repulsive_bh(t: MortonQuadtree, y, theta: float,
@@ -91,12 +101,13 @@ def repulsive_bh(t: MortonQuadtree, y, theta: float,
     n = pts.shape[0]
     if n != t.n_points:
         raise ValueError(f"tree is over {t.n_points} points, embedding has {n}")
-    _check_out(out, dt, "repulsive_bh")
+    res = _Out(out.rep, dt)
     lib = _lib.load()
     ws = _lib.workspace(lib.bh_repulsive_workspace_bytes(n))
     call(_lib.fn("bh_repulsive", dt), t.arrays.sref(), ptr(t.bounds),
-         float(theta), ptr(pts), 0, n, 0, ptr(out.rep), ptr(out.z_partial),
+         float(theta), ptr(pts), 0, n, 0, ptr(res.t), ptr(out.z_partial),
          None, ptr(out.z_dev), None, ptr(ws), ws.numel(), stream())
+    res.done()
 
 
 def repulsive_counts(t: MortonQuadtree, theta: float) -> np.ndarray:
@@ -121,8 +132,9 @@ def repulsive_exact(y, out: GradientBuffers) -> None:
     n = pts.shape[0]
     if n < 2:
         raise ValueError("need at least 2 points")
-    _check_out(out, pts.dtype, "repulsive_exact")
+    res = _Out(out.rep, pts.dtype)
     lib = _lib.load()
     ws = _lib.workspace(lib.bh_repulsive_exact_workspace_bytes(n))
-    call(_lib.fn("bh_repulsive_exact", pts.dtype), ptr(pts), n, ptr(out.rep),
+    call(_lib.fn("bh_repulsive_exact", pts.dtype), ptr(pts), n, ptr(res.t),
          ptr(out.z_partial), ptr(out.z_dev), ptr(ws), ws.numel(), stream())
+    res.done()
