@@ -304,6 +304,8 @@ class Engine:
         # apart for the per-stage breakdown unless fuse_timed is set
         self.fuse = True
         self.fuse_timed = False
+        # sharded fast path: attractive + its all-gather on the side stream
+        self.shard_overlap = True
         self.launches = 0  # library kernels enqueued by run() (bench claim)
         # True: full chunks of the fast path replay one graph_chunk-iteration
         # graph (+0.2% device time, but capturing 25-iteration graphs for the
@@ -355,6 +357,17 @@ class Engine:
         rec(0)
         call(self.fn("bh_morton"), ptr(y), n, ptr(self.bounds), cb, 1,
              ptr(self.codes), st)
+        side = (self.shard is not None and self.shard_overlap
+                and ev is None)
+        if side:
+            # sharded fast path: this rank's attractive rows and their
+            # all-gather run on the side stream under the replicated tree
+            # build (dist.py)
+            self.fork_ev.record(torch.cuda.current_stream())
+            with torch.cuda.stream(self.side):
+                self.side.wait_event(self.fork_ev)
+                self.shard.attractive_side(self)
+                self.join_ev.record(self.side)
         if self.shard is None and self.overlap:
             # fork: the memory-bound CSR sweep needs only the centred Y, so
             # it runs on a side stream under the latency-bound sort / tree /
@@ -402,6 +415,9 @@ class Engine:
                 torch.cuda.current_stream().wait_event(self.join_ev)
             rec(5)
             rep, rep_rank = self.rep, None
+        elif side:
+            rep, rep_rank = self.shard.repulsive(self, rec, st)
+            torch.cuda.current_stream().wait_event(self.join_ev)
         else:
             rep, rep_rank = self.shard.forces(self, rec, st)
         call(self.fn("bh_update"), ptr(y), ptr(self.v), ptr(self.g),
@@ -428,7 +444,8 @@ class Engine:
     def _graph1(self):
         """One iteration without timing events (the fast path: replayed
         back to back, the host only syncs at chunk boundaries)."""
-        key = ("fast", self.csr_key, self.overlap, self._fused(False))
+        key = ("fast", self.csr_key, self.overlap, self._fused(False),
+               self.shard_overlap)
         if key not in self.graphs:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.main):
@@ -440,7 +457,8 @@ class Engine:
         """graph_chunk iterations in one graph without timing events: one
         graph launch per chunk instead of one per iteration."""
         k = self.cfg.graph_chunk
-        key = ("fastk", k, self.csr_key, self.overlap, self._fused(False))
+        key = ("fastk", k, self.csr_key, self.overlap, self._fused(False),
+               self.shard_overlap)
         if key not in self.graphs:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.main):
