@@ -171,6 +171,9 @@ class TreeArrays:
         return C.byref(self.struct)
 
     def build(self, pts: torch.Tensor, st=None):
+        if pts.dtype != self.dtype or tuple(pts.shape) != (self.n, 2):
+            raise ValueError(f"tree is for ({self.n}, 2) {self.dtype} points, "
+                             f"got {tuple(pts.shape)} {pts.dtype}")
         call("bh_build_tree", self.sref(), ptr(pts), ptr(self.ws),
              self.ws.numel(), st or stream())
 
