@@ -242,7 +242,7 @@ def reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "it/s",
         "n_gpus": world, "steps": steps, "warmup": w,
         "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic", "config": config_dict(args, n, int(prob["col"].shape[0])),
         "cpu_baseline": {"value": v, "unit": "it/s", "cores": threads,
                          "kind": "port",
