@@ -196,7 +196,7 @@ int bh_attractive(const int64_t *row_ptr, const int32_t *col,
  * t - t_begin (sorted_out = 1): rep (float32 pairs), zpart (float64,
  * optional), counts (optional, 4 int32: internal visits, leaf-node visits,
  * leaf points touched, accepted).  zblock (optional; else in ws) receives
- * one f64 partial of Z per 256 consecutive sorted points; z_out (optional)
+ * one f64 partial of Z per 128 consecutive sorted points; z_out (optional)
  * their fixed-order sum (the same reduction bh_sum_partials applies, so Z
  * does not depend on how ranges are split across GPUs). */
 size_t bh_repulsive_workspace_bytes(int64_t n);
@@ -235,7 +235,7 @@ int bh_repulsive_f64(const bh_tree_t *tree, const bh_bounds_t *bounds,
 /* *out = fixed-order sum of n per-CTA Z partials (see bh_repulsive). */
 int bh_sum_partials(const double *x, int64_t n, double *out,
                     bh_stream_t stream);
-#define BH_REP_POINTS_PER_PARTIAL 256
+#define BH_REP_POINTS_PER_PARTIAL 128
 
 /* ---- exact O(N^2) repulsion (forces.py:153-182) -------------------------- */
 size_t bh_repulsive_exact_workspace_bytes(int64_t n);

@@ -164,9 +164,10 @@ struct RepArgs {
 };
 
 #ifndef BH_REP_MIN_BLOCKS
-// 5 CTAs x 8 warps per SM (48 registers): measured 1.23 ms vs 1.33 ms (4),
-// 1.44 ms (3), 2.29 ms (6, heavy spills) at C3 iteration 600
-#define BH_REP_MIN_BLOCKS 5
+// 9 CTAs x 4 warps per SM (56 registers).  With 8-warp CTAs: 5 per SM
+// (48 registers) measured 1.23 ms vs 1.33 ms (4), 1.44 ms (3), 2.29 ms (6,
+// heavy spills) at C3 iteration 600
+#define BH_REP_MIN_BLOCKS 9
 #endif
 
 // CTA `bid` of the `nblk` traversal CTAs: points t_begin + 256 bid + [0, 256).
@@ -271,11 +272,13 @@ struct AttArgs {
     float2 *__restrict__ attr;
 };
 
-// CTA `bid` of `nblk` sweeping CTAs (256 threads): row batches of 256 / G
-// rows, batch b handled by CTA b mod nblk.
-template <int G, bool PADDED>
+// CTA `bid` of `nblk` sweeping CTAs of THREADS threads: row batches of
+// THREADS / G rows, batch b handled by CTA b mod nblk.
+template <int G, bool PADDED, int THREADS>
 __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
                                           int64_t nblk) {
+    static_assert(THREADS % G == 0, "whole row groups per CTA");
+    constexpr int kRows = THREADS / G;
     const int64_t *__restrict__ rp = A.rp;
     const int32_t *__restrict__ col = A.col;
     const float *__restrict__ val = A.val;
@@ -287,8 +290,8 @@ __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
                                     : 1.0f)
                              : A.exag_param;
     const int gl = threadIdx.x % G;
-    for (int64_t r0 = A.row_begin + bid * (256 / G); r0 < row_end;
-         r0 += nblk * (256 / G)) {
+    for (int64_t r0 = A.row_begin + bid * kRows; r0 < row_end;
+         r0 += nblk * kRows) {
     const int64_t row = r0 + threadIdx.x / G;
     const bool ok = row < row_end;
     int64_t s = 0, e = 0;
@@ -345,7 +348,7 @@ __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
 
 template <int G, bool PADDED>
 __global__ void __launch_bounds__(256) k_attractive(const AttArgs A) {
-    att_block<G, PADDED>(A, blockIdx.x, gridDim.x);
+    att_block<G, PADDED, 256>(A, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -362,7 +365,7 @@ k_forces(const RepArgs R, const AttArgs A, int64_t nr, int64_t na) {
     const int64_t b = blockIdx.x, nb = nr + na;
     const int64_t before = (b * na) / nb, upto = ((b + 1) * na) / nb;
     if (upto > before)
-        att_block<G, PADDED>(A, before, na);
+        att_block<G, PADDED, kRepThreads>(A, before, na);
     else
         rep_block<D, false, false>(R, b - upto, nr);
 }
@@ -608,7 +611,7 @@ extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
     const int64_t nr = rep_grid(t_end - t_begin);
     const int64_t na = std::max<int64_t>(
         1, std::min<int64_t>((nr + ratio - 1) / ratio,
-                             bh_blocks(row_end - row_begin, 256 / G)));
+                             bh_blocks(row_end - row_begin, kRepThreads / G)));
     char *w = (char *)ws;
     if (!zblock) zblock = (double *)w;
     unsigned *ticket = (unsigned *)(w + bh_align(sizeof(double) * nr));

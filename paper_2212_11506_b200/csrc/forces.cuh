@@ -7,8 +7,16 @@
 
 namespace bh {
 
-constexpr int kRepWarps = 8;
+#ifndef BH_REP_WARPS
+// 4 warps per traversal CTA at 9 CTAs/SM (56 registers, no spills): the
+// fused force pass interleaves traversal and sweep CTAs more finely than
+// with 8-warp CTAs (1.705 vs 1.775 ms at C3 iteration 600)
+#define BH_REP_WARPS 4
+#endif
+constexpr int kRepWarps = BH_REP_WARPS;
 constexpr int kRepThreads = kRepWarps * 32;
+static_assert(kRepThreads == BH_REP_POINTS_PER_PARTIAL,
+              "one Z partial per traversal CTA (include/bhtsne_b200.h)");
 
 static inline int rep_grid(int64_t npts) { return bh_blocks(npts, kRepThreads); }
 
@@ -66,7 +74,7 @@ struct Acc64 {
     double z, r0, r1;
 };
 
-// Z: per-CTA partial (256 points in Morton order), then one fixed-order
+// Z: per-CTA partial (128 points in Morton order), then one fixed-order
 // warp reduction over all CTA partials (fixed_sum) -- the same reduction the
 // multi-GPU path applies to the gathered partials, so Z is bitwise
 // independent of the GPU count.  No CTA-wide barrier: the

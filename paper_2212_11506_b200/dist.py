@@ -9,13 +9,13 @@ work is sharded contiguously:
 * attraction: CSR rows [r0, r1) (point ids).
 
 One exchange per iteration: an all-gather of the attractive rows, the
-sorted-order repulsive forces and the per-256-point Z partials.  Every rank
+sorted-order repulsive forces and the per-128-point Z partials.  Every rank
 then runs the (cheap, elementwise) update for all N points on identical
 inputs, so Y stays replicated without a separate Y all-gather.  In the
 untimed fast path the attractive rows and their all-gather run on a side
 stream (with their own communicator) under the replicated tree build, so
 only the repulsive exchange remains on the critical path.  Ranges are
-multiples of 256 points, so the gathered Z partials are exactly the blocks
+multiples of 128 points, so the gathered Z partials are exactly the blocks
 a single GPU produces and Z -- hence the whole trajectory -- is bitwise
 independent of the GPU count.
 
@@ -29,7 +29,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
-POINTS_PER_PARTIAL = 256  # BH_REP_POINTS_PER_PARTIAL (include/bhtsne_b200.h)
+POINTS_PER_PARTIAL = 128  # BH_REP_POINTS_PER_PARTIAL (include/bhtsne_b200.h)
 
 
 @dataclass(frozen=True)

@@ -136,3 +136,13 @@ def test_morton_interleave_host_helper():
     from paper_2212_11506_b200 import morton_interleave
     assert morton_interleave(3, 7) == 47
     assert morton_interleave(0, 0) == 0
+
+
+def test_partial_granularity_matches_header():
+    """dist.ShardPlan aligns ranges to the traversal CTA's Z partial size,
+    which the library static_asserts against the header macro."""
+    import re
+    from paper_2212_11506_b200.dist import POINTS_PER_PARTIAL
+    with open(HEADER) as fh:
+        m = re.search(r"#define BH_REP_POINTS_PER_PARTIAL (\d+)", fh.read())
+    assert m and int(m.group(1)) == POINTS_PER_PARTIAL

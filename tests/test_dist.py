@@ -47,7 +47,7 @@ def problem():
 
 def shard_forces(o, y, ro, co, va, plan):
     """What one rank's kernels produce: attr rows, sorted-order rep, Z
-    partials of its 256-point blocks."""
+    partials of its POINTS_PER_PARTIAL-point blocks."""
     n = y.shape[0]
     t = o.build_tree(y, code_bits=32)          # replicated tree
     a0, a1 = o.attractive(ro, co, va, y)
