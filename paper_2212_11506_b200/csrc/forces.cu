@@ -602,15 +602,18 @@ extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
     BH_REQUIRE(ws_bytes >= bh_repulsive_workspace_bytes(t_end - t_begin),
                "repulsive workspace too small");
     // sweeping CTAs per traversal CTA (tuning knob BH_FUSE_RATIO = nr / na)
-    static const int ratio = [] {
+    static const double ratio = [] {
         const char *s = getenv("BH_FUSE_RATIO");
-        const int r = s ? atoi(s) : 2;
-        return r >= 1 ? r : 2;
+        const double r = s ? atof(s) : 2.0;
+        return r > 0.0 ? r : 2.0;
     }();
-    constexpr int G = 16;
+#ifndef BH_FUSE_G
+#define BH_FUSE_G 16
+#endif
+    constexpr int G = BH_FUSE_G;
     const int64_t nr = rep_grid(t_end - t_begin);
     const int64_t na = std::max<int64_t>(
-        1, std::min<int64_t>((nr + ratio - 1) / ratio,
+        1, std::min<int64_t>((int64_t)ceil((double)nr / ratio),
                              bh_blocks(row_end - row_begin, kRepThreads / G)));
     char *w = (char *)ws;
     if (!zblock) zblock = (double *)w;
