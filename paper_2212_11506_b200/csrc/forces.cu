@@ -247,6 +247,9 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
 template <int D, bool COUNT, bool QUERY>
 __global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
 k_repulsive(const RepArgs A) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     rep_block<D, COUNT, QUERY>(A, blockIdx.x, gridDim.x);
 }
 // Sum of gathered per-CTA Z partials into *out (one warp, fixed order).
@@ -348,6 +351,9 @@ __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
 
 template <int G, bool PADDED>
 __global__ void __launch_bounds__(256) k_attractive(const AttArgs A) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     att_block<G, PADDED, 256>(A, blockIdx.x, gridDim.x);
 }
 
@@ -362,6 +368,9 @@ __global__ void __launch_bounds__(256) k_attractive(const AttArgs A) {
 template <int D, int G, bool PADDED>
 __global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
 k_forces(const RepArgs R, const AttArgs A, int64_t nr, int64_t na) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     const int64_t b = blockIdx.x, nb = nr + na;
     const int64_t before = (b * na) / nb, upto = ((b + 1) * na) / nb;
     if (upto > before)
@@ -510,7 +519,8 @@ extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
                     (const float2 *)y_query, bounds, t->status, theta, t_begin,
                     t_end, sorted_out, (float2 *)rep, zpart, (int4 *)counts,
                     zblock, ticket, z_out};
-#define BH_REP_LAUNCH(D, CNT, Q) k_repulsive<D, CNT, Q><<<grid, kRepThreads, 0, st>>>(A)
+#define BH_REP_LAUNCH(D, CNT, Q)                                              \
+    BH_LAUNCH("k_repulsive", (k_repulsive<D, CNT, Q>), grid, kRepThreads, 0, st, A)
 #define BH_REP_LAUNCH2(D)                                                     \
     if (y_query) {                                                            \
         if (counts) BH_REP_LAUNCH(D, true, true); else BH_REP_LAUNCH(D, false, true); \
@@ -560,9 +570,11 @@ extern "C" int bh_attractive(const int64_t *row_ptr, const int32_t *col,
     {                                                                         \
         const int grid = bh_blocks(row_end - row_begin, 256 / G);             \
         if (padded)                                                           \
-            k_attractive<G, true><<<grid, 256, 0, st>>>(A);                   \
+            BH_LAUNCH("k_attractive", (k_attractive<G, true>), grid, 256, 0,  \
+                      st, A);                                                 \
         else                                                                  \
-            k_attractive<G, false><<<grid, 256, 0, st>>>(A);                  \
+            BH_LAUNCH("k_attractive", (k_attractive<G, false>), grid, 256, 0, \
+                      st, A);                                                 \
     }
     switch (g_env) {
         case 4: BH_ATTR(4) break;
@@ -628,9 +640,11 @@ extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
     const unsigned grid = (unsigned)(nr + na);
 #define BH_FORCES(D)                                                          \
     if (padded)                                                               \
-        k_forces<D, G, true><<<grid, kRepThreads, 0, st>>>(R, A, nr, na);     \
+        BH_LAUNCH("k_forces", (k_forces<D, G, true>), grid, kRepThreads, 0,   \
+                  st, R, A, nr, na);                                          \
     else                                                                      \
-        k_forces<D, G, false><<<grid, kRepThreads, 0, st>>>(R, A, nr, na);
+        BH_LAUNCH("k_forces", (k_forces<D, G, false>), grid, kRepThreads, 0,  \
+                  st, R, A, nr, na);
     if (t->code_bits == 32) {
         BH_FORCES(16)
     } else if (t->code_bits == 64) {

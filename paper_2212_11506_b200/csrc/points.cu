@@ -191,6 +191,9 @@ template <typename T>
 __global__ void __launch_bounds__(kPtThreads)
 k_bounds(const p2_t<T> *__restrict__ y, int64_t n, int code_bits,
          bh_bounds_t *out, PtPartial<T> *part, unsigned *ticket) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     MinMax<T> m;
     mm_init(m);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -223,6 +226,9 @@ k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
          int apply_shift,
          typename std::conditional<BITS == 32, uint32_t, uint64_t>::type
              *__restrict__ codes) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     const double root0 = b->root0, root1 = b->root1, scale = b->scale;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -320,6 +326,9 @@ k_update(p2_t<T> *__restrict__ y, p2_t<T> *__restrict__ v,
          const p2_t<T> *__restrict__ rep, const int32_t *__restrict__ rep_rank,
          int64_t n, bh_sched_t *sched, bh_bounds_t *out, int code_bits,
          PtPartial<T> *part, unsigned *ticket) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     const int it = sched->iteration;
     sched_t<T> S;
     S.init(sched, it);
@@ -367,6 +376,9 @@ k_update(p2_t<T> *__restrict__ y, p2_t<T> *__restrict__ v,
 template <typename T>
 __global__ void k_center(p2_t<T> *__restrict__ y, int64_t n,
                          const bh_bounds_t *__restrict__ b) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         y[i] = shifted(y[i], b);
@@ -391,9 +403,8 @@ static int bounds_impl(const T *y, int64_t n, int code_bits, bh_bounds_t *out,
     char *w = (char *)ws;
     PtPartial<T> *part = (PtPartial<T> *)w;
     unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial<T>) * grid));
-    k_bounds<T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
-        (const p2_t<T> *)y, n, code_bits, out, part, ticket);
-    BH_CHECK_LAUNCH("k_bounds");
+    BH_LAUNCH("k_bounds", k_bounds<T>, grid, kPtThreads, 0, bh_cs(stream),
+              (const p2_t<T> *)y, n, code_bits, out, part, ticket);
     return BH_OK;
 }
 
@@ -404,14 +415,15 @@ static int morton_impl(T *y, int64_t n, const bh_bounds_t *bounds,
     BH_REQUIRE(n >= 1, "need at least one point");
     int grid = pt_grid(n);
     if (code_bits == 32)
-        k_morton<32, T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
-            (p2_t<T> *)y, n, bounds, apply_shift, (uint32_t *)codes);
+        BH_LAUNCH("k_morton", (k_morton<32, T>), grid, kPtThreads, 0,
+                  bh_cs(stream), (p2_t<T> *)y, n, bounds, apply_shift,
+                  (uint32_t *)codes);
     else if (code_bits == 64)
-        k_morton<64, T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
-            (p2_t<T> *)y, n, bounds, apply_shift, (uint64_t *)codes);
+        BH_LAUNCH("k_morton", (k_morton<64, T>), grid, kPtThreads, 0,
+                  bh_cs(stream), (p2_t<T> *)y, n, bounds, apply_shift,
+                  (uint64_t *)codes);
     else
         return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
-    BH_CHECK_LAUNCH("k_morton");
     return BH_OK;
 }
 
@@ -426,11 +438,10 @@ static int update_impl(T *y, T *v, T *g, const T *attr, const T *rep,
     char *w = (char *)ws;
     PtPartial<T> *part = (PtPartial<T> *)w;
     unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial<T>) * grid));
-    k_update<T><<<grid, kPtThreads, 0, bh_cs(stream)>>>(
-        (p2_t<T> *)y, (p2_t<T> *)v, (p2_t<T> *)g, (const p2_t<T> *)attr,
-        (const p2_t<T> *)rep, rep_rank, n, sched, bounds_out, code_bits, part,
-        ticket);
-    BH_CHECK_LAUNCH("k_update");
+    BH_LAUNCH("k_update", k_update<T>, grid, kPtThreads, 0, bh_cs(stream),
+              (p2_t<T> *)y, (p2_t<T> *)v, (p2_t<T> *)g, (const p2_t<T> *)attr,
+              (const p2_t<T> *)rep, rep_rank, n, sched, bounds_out, code_bits,
+              part, ticket);
     return BH_OK;
 }
 
@@ -486,17 +497,15 @@ extern "C" int bh_update_f64(double *y, double *v, double *g,
 
 extern "C" int bh_center(float *y, int64_t n, const bh_bounds_t *bounds,
                          bh_stream_t stream) {
-    k_center<float><<<pt_grid(n), kPtThreads, 0, bh_cs(stream)>>>(
-        (float2 *)y, n, bounds);
-    BH_CHECK_LAUNCH("k_center");
+    BH_LAUNCH("k_center", k_center<float>, pt_grid(n), kPtThreads, 0,
+              bh_cs(stream), (float2 *)y, n, bounds);
     return BH_OK;
 }
 
 extern "C" int bh_center_f64(double *y, int64_t n, const bh_bounds_t *bounds,
                              bh_stream_t stream) {
-    k_center<double><<<pt_grid(n), kPtThreads, 0, bh_cs(stream)>>>(
-        (double2 *)y, n, bounds);
-    BH_CHECK_LAUNCH("k_center");
+    BH_LAUNCH("k_center", k_center<double>, pt_grid(n), kPtThreads, 0,
+              bh_cs(stream), (double2 *)y, n, bounds);
     return BH_OK;
 }
 

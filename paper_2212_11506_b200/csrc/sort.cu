@@ -35,10 +35,25 @@ struct SortCfg {
     static_assert(SMEM <= 48 * 1024, "tile must fit the default smem limit");
 };
 
+// Digit histograms of all passes, and the reset of the passes' control words
+// (look-back status, tile counters) -- no memset node in the iteration, so
+// the whole chain is kernel-to-kernel (PDL).  Counts accumulate into one of
+// two buffers chosen by a call epoch; the last CTA publishes them to `hist`,
+// and zeroes the other buffer for the next call.
 template <typename K>
 __global__ void __launch_bounds__(256)
 k_sort_hist(const K *__restrict__ keys, int64_t n, int passes,
-            uint32_t *__restrict__ hist) {
+            uint32_t *__restrict__ hist, uint32_t *__restrict__ acc2,
+            uint32_t *__restrict__ epoch, unsigned *__restrict__ ticket,
+            uint32_t *__restrict__ zero, int64_t zero_words) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+    const uint32_t ep = *(volatile uint32_t *)epoch;
+    uint32_t *acc = acc2 + (size_t)(ep & 1u) * 8 * 256;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+         i < zero_words; i += (int64_t)gridDim.x * blockDim.x)
+        zero[i] = 0u;
+
     __shared__ uint32_t sh[8][256];
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
@@ -74,7 +89,23 @@ k_sort_hist(const K *__restrict__ keys, int64_t n, int passes,
     __syncthreads();
     for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
         uint32_t c = (&sh[0][0])[i];
-        if (c) atomicAdd(&hist[i], c);
+        if (c) atomicAdd(&acc[i], c);
+    }
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint32_t *other = acc2 + (size_t)((ep + 1u) & 1u) * 8 * 256;
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+        hist[i] = __ldcg(&acc[i]);
+        other[i] = 0u;
+    }
+    if (threadIdx.x == 0) {
+        *epoch = ep + 1u;
+        *ticket = 0u;
     }
 }
 
@@ -84,6 +115,9 @@ k_sort_pass(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
             K *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
             int shift, const uint32_t *__restrict__ hist,
             uint32_t *__restrict__ status, uint32_t *__restrict__ tile_ctr) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     constexpr int IPT = SortCfg<K>::IPT, TILE = SortCfg<K>::TILE;
     extern __shared__ __align__(16) unsigned char smem[];
     K *s_keys = (K *)smem;
@@ -203,7 +237,7 @@ k_sort_pass(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
 }
 
 struct SortLayout {
-    size_t keys_a, vals_a, keys_b, vals_b, hist, ctr, status, total;
+    size_t keys_a, vals_a, keys_b, vals_b, hist, ctr, status, acc, misc, total;
     int passes;
     int64_t tiles;
 };
@@ -226,6 +260,8 @@ static SortLayout sort_layout(int64_t n, int key_bits) {
     L.hist = take(4 * 256 * L.passes);
     L.ctr = take(4 * L.passes);
     L.status = take(4 * 256 * (size_t)L.tiles * L.passes);
+    L.acc = take(4 * 2 * 8 * 256);  // two histogram accumulators
+    L.misc = take(16);              // epoch, ticket
     L.total = off;
     return L;
 }
@@ -245,12 +281,15 @@ static int sort_impl(const K *keys, const uint32_t *vals, int64_t n,
     uint32_t *hist = (uint32_t *)(w + L.hist);
     uint32_t *ctr = (uint32_t *)(w + L.ctr);
     uint32_t *status = (uint32_t *)(w + L.status);
-    cudaError_t e = cudaMemsetAsync(w + L.hist, 0, L.total - L.hist, st);
-    if (e != cudaSuccess) return cuda_status(e, "sort memset");
+    uint32_t *misc = (uint32_t *)(w + L.misc);
     int hb = bh_blocks(n, 256 * 16);
     if (hb > kSMs * 4) hb = kSMs * 4;
-    k_sort_hist<K><<<hb, 256, 0, st>>>(keys, n, L.passes, hist);
-    BH_CHECK_LAUNCH("k_sort_hist");
+    // tile counters and look-back status are contiguous: [ctr, status)
+    const int64_t zero_words = (int64_t)((L.status - L.ctr) / 4 +
+                                         (size_t)256 * L.tiles * L.passes);
+    BH_LAUNCH("k_sort_hist", k_sort_hist<K>, hb, 256, 0, st, keys, n,
+              L.passes, hist, (uint32_t *)(w + L.acc), misc, misc + 1, ctr,
+              zero_words);
     K *kb[2] = {(K *)(w + L.keys_a), (K *)(w + L.keys_b)};
     uint32_t *vb[2] = {(uint32_t *)(w + L.vals_a), (uint32_t *)(w + L.vals_b)};
     for (int p = 0; p < L.passes; p++) {
@@ -258,10 +297,10 @@ static int sort_impl(const K *keys, const uint32_t *vals, int64_t n,
         const uint32_t *vi = p == 0 ? vals : vb[(p - 1) & 1];
         K *ko = p == L.passes - 1 ? out_keys : kb[p & 1];
         uint32_t *vo = p == L.passes - 1 ? out_vals : vb[p & 1];
-        k_sort_pass<K><<<(int)L.tiles, kSortThreads, SortCfg<K>::SMEM, st>>>(
-            ki, vi, ko, vo, n, 8 * p, hist + 256 * p,
-            status + (size_t)256 * L.tiles * p, ctr + p);
-        BH_CHECK_LAUNCH("k_sort_pass");
+        BH_LAUNCH("k_sort_pass", k_sort_pass<K>, (unsigned)L.tiles,
+                  kSortThreads, SortCfg<K>::SMEM, st, ki, vi, ko, vo, n, 8 * p,
+                  (const uint32_t *)(hist + 256 * p),
+                  status + (size_t)256 * L.tiles * p, ctr + p);
     }
     return BH_OK;
 }

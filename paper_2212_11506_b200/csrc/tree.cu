@@ -48,6 +48,9 @@ template <typename K, int D>
 __global__ void __launch_bounds__(kTreeThreads)
 k_tree_count(const K *__restrict__ sc, int64_t n,
              uint32_t *__restrict__ blk_counts) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     __shared__ uint32_t s_cnt[kTreeWarps][D + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t cnt[D + 1];
@@ -83,6 +86,9 @@ __global__ void __launch_bounds__(1024)
 k_tree_scan(const uint32_t *__restrict__ blk_counts, int nblk,
             uint32_t *__restrict__ blk_off, int32_t *__restrict__ level_off,
             int64_t capacity, int32_t *__restrict__ status) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     __shared__ uint32_t s_tot[D + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int d = warp; d <= D; d += 32) {
@@ -126,6 +132,9 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
             int32_t *__restrict__ parent, int32_t *__restrict__ node_start,
             int32_t *__restrict__ leaf_end, p2_t<T> *__restrict__ ys,
             int32_t *__restrict__ rank, const int32_t *__restrict__ status) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     using Rec = NodeRec<T>;
     if (*status != BH_OK) return;
     __shared__ uint32_t s_bal[kTreeWarps][D + 1];
@@ -253,6 +262,9 @@ k_summarize_level(void *__restrict__ node, const int32_t *__restrict__ parent,
                   const p2_t<T> *__restrict__ ys,
                   const int32_t *__restrict__ level_off, int d, int D,
                   const int32_t *__restrict__ status) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     if (*status != BH_OK) return;
     const int32_t lo = level_off[d], hi = level_off[d + 1];
     const int32_t hi_next = d < D ? level_off[d + 2] : hi;
@@ -273,6 +285,9 @@ k_summarize_top(void *__restrict__ node, const int32_t *__restrict__ parent,
                 const p2_t<T> *__restrict__ ys,
                 const int32_t *__restrict__ level_off, int dtop, int D,
                 const int32_t *__restrict__ status) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
     if (*status != BH_OK) return;
     for (int d = dtop; d >= 0; d--) {
         const int32_t lo = level_off[d], hi = level_off[d + 1];
@@ -305,16 +320,14 @@ static int build_impl(const bh_tree_t *t, const void *y, void *ws,
     char *w = (char *)ws;
     uint32_t *cnt = (uint32_t *)(w + L.counts), *off = (uint32_t *)(w + L.offs);
     const K *sc = (const K *)t->sorted_codes;
-    k_tree_count<K, D><<<L.nblk, kTreeThreads, 0, st>>>(sc, t->n_points, cnt);
-    BH_CHECK_LAUNCH("k_tree_count");
-    k_tree_scan<D><<<1, 1024, 0, st>>>(cnt, L.nblk, off, t->level_off,
+    BH_LAUNCH("k_tree_count", (k_tree_count<K, D>), L.nblk, kTreeThreads, 0,
+              st, sc, t->n_points, cnt);
+    BH_LAUNCH("k_tree_scan", k_tree_scan<D>, 1, 1024, 0, st, cnt, L.nblk, off, t->level_off,
                                        t->node_capacity, t->status);
-    BH_CHECK_LAUNCH("k_tree_scan");
-    k_tree_emit<K, D, T><<<L.nblk, kTreeThreads, 0, st>>>(
+    BH_LAUNCH("k_tree_emit", (k_tree_emit<K, D, T>), L.nblk, kTreeThreads, 0, st,
         sc, t->order, (const p2_t<T> *)y, t->n_points, off, t->level_off,
         (void *)t->node, t->parent, t->node_start, t->leaf_end,
         (p2_t<T> *)t->ys, t->rank, t->status);
-    BH_CHECK_LAUNCH("k_tree_emit");
     return BH_OK;
 }
 
@@ -369,25 +382,27 @@ extern "C" int bh_summarize(const bh_tree_t *t, void *ws, size_t ws_bytes,
     const int dtop = std::min(top, D);
     for (int d = D; d > dtop; d--) {
         if (tree_f64(t))
-            k_summarize_level<double><<<grid, kSumThreads, 0, bh_cs(stream)>>>(
-                (void *)t->node, t->parent, t->leaf_end,
-                (const double2 *)t->ys, t->level_off, d, D, t->status);
+            BH_LAUNCH("k_summarize_level", k_summarize_level<double>, grid,
+                      kSumThreads, 0, bh_cs(stream), (void *)t->node, t->parent,
+                      t->leaf_end, (const double2 *)t->ys, t->level_off, d, D,
+                      t->status);
         else
-            k_summarize_level<float><<<grid, kSumThreads, 0, bh_cs(stream)>>>(
-                (void *)t->node, t->parent, t->leaf_end, (const float2 *)t->ys,
-                t->level_off, d, D, t->status);
-        BH_CHECK_LAUNCH("k_summarize_level");
+            BH_LAUNCH("k_summarize_level", k_summarize_level<float>, grid,
+                      kSumThreads, 0, bh_cs(stream), (void *)t->node, t->parent,
+                      t->leaf_end, (const float2 *)t->ys, t->level_off, d, D,
+                      t->status);
     }
     if (dtop >= 0) {
         if (tree_f64(t))
-            k_summarize_top<double><<<1, kSumTopThreads, 0, bh_cs(stream)>>>(
-                (void *)t->node, t->parent, t->leaf_end,
-                (const double2 *)t->ys, t->level_off, dtop, D, t->status);
+            BH_LAUNCH("k_summarize_top", k_summarize_top<double>, 1,
+                      kSumTopThreads, 0, bh_cs(stream), (void *)t->node,
+                      t->parent, t->leaf_end, (const double2 *)t->ys,
+                      t->level_off, dtop, D, t->status);
         else
-            k_summarize_top<float><<<1, kSumTopThreads, 0, bh_cs(stream)>>>(
-                (void *)t->node, t->parent, t->leaf_end, (const float2 *)t->ys,
-                t->level_off, dtop, D, t->status);
-        BH_CHECK_LAUNCH("k_summarize_top");
+            BH_LAUNCH("k_summarize_top", k_summarize_top<float>, 1,
+                      kSumTopThreads, 0, bh_cs(stream), (void *)t->node,
+                      t->parent, t->leaf_end, (const float2 *)t->ys,
+                      t->level_off, dtop, D, t->status);
     }
     return BH_OK;
 }
