@@ -235,7 +235,9 @@ int bh_repulsive_f64(const bh_tree_t *tree, const bh_bounds_t *bounds,
 /* *out = fixed-order sum of n per-CTA Z partials (see bh_repulsive). */
 int bh_sum_partials(const double *x, int64_t n, double *out,
                     bh_stream_t stream);
+#ifndef BH_REP_POINTS_PER_PARTIAL
 #define BH_REP_POINTS_PER_PARTIAL 128
+#endif
 
 /* ---- exact O(N^2) repulsion (forces.py:153-182) -------------------------- */
 size_t bh_repulsive_exact_workspace_bytes(int64_t n);
