@@ -232,6 +232,14 @@ int bh_repulsive_f64(const bh_tree_t *tree, const bh_bounds_t *bounds,
                      int64_t t_end, int sorted_out, double *rep, double *zpart,
                      double *zblock, double *z_out, int32_t *counts, void *ws,
                      size_t ws_bytes, bh_stream_t stream);
+int bh_forces_f64(const bh_tree_t *tree, const bh_bounds_t *bounds,
+                  double theta, int64_t t_begin, int64_t t_end, int sorted_out,
+                  double *rep, double *zblock, double *z_out, void *ws,
+                  size_t ws_bytes, const int64_t *row_ptr, const int32_t *col,
+                  const double *val, int64_t n_rows, int padded,
+                  const double *y, int64_t row_begin, int64_t row_end,
+                  double exaggeration, const bh_sched_t *sched, double *attr,
+                  bh_stream_t stream);
 /* *out = fixed-order sum of n per-CTA Z partials (see bh_repulsive). */
 int bh_sum_partials(const double *x, int64_t n, double *out,
                     bh_stream_t stream);

@@ -84,6 +84,9 @@ SIGNATURES = {
                    _P, _P, _P, _P, _SZ, _P, _P, _P, _I64, C.c_int, _P, _I64,
                    _I64, C.c_float, _P, _P, _P], C.c_int),
     "bh_sum_partials": ([_P, _I64, _P, _P], C.c_int),
+    "bh_forces_f64": ([C.POINTER(TreeStruct), _P, C.c_double, _I64, _I64,
+                       C.c_int, _P, _P, _P, _P, _SZ, _P, _P, _P, _I64, C.c_int,
+                       _P, _I64, _I64, C.c_double, _P, _P, _P], C.c_int),
     "bh_attractive_f64": ([_P, _P, _P, _I64, C.c_int, _P, _I64, _I64,
                            C.c_double, _P, _P, _P], C.c_int),
     "bh_repulsive_f64": ([C.POINTER(TreeStruct), _P, C.c_double, _P, _I64,

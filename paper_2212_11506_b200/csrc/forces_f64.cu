@@ -108,9 +108,10 @@ __device__ __forceinline__ uint4 side2_entry(uint32_t info, uint32_t msk,
     return make_uint4(info, msk, (uint32_t)b, (uint32_t)(b >> 32));
 }
 
+// Traversal CTA `bid` of `nblk`: sorted positions t_begin + 128 bid + [0, 128).
 template <int D, bool COUNT, bool QUERY>
-__global__ void __launch_bounds__(kRepThreads)
-k_repulsive64(const RepArgs64 A) {
+__device__ __forceinline__ void rep_block64(const RepArgs64 &A, int64_t bid,
+                                            int64_t nblk) {
     constexpr int CAP = 3 * D + 2;
     __shared__ uint4 s_stack[kRepWarps][CAP];
     __shared__ double s_z[kRepWarps];
@@ -118,7 +119,6 @@ k_repulsive64(const RepArgs64 A) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-    const int64_t bid = blockIdx.x, nblk = gridDim.x;
     const int64_t t = A.t_begin + (bid * kRepWarps + warp) * 32 + lane;
     const bool valid = t < A.t_end && *A.status == BH_OK;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
@@ -176,20 +176,44 @@ k_repulsive64(const RepArgs64 A) {
                A.z_out);
 }
 
-// Attractive sweep, G lanes per row (forces.py:56-71 in f64).
-template <int G, bool PADDED>
-__global__ void __launch_bounds__(256)
-k_attractive64(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-               const double *__restrict__ val, const double2 *__restrict__ y,
-               int64_t row_begin, int64_t row_end, double exag_param,
-               const bh_sched_t *__restrict__ sched, double2 *__restrict__ attr) {
+template <int D, bool COUNT, bool QUERY>
+__global__ void __launch_bounds__(kRepThreads)
+k_repulsive64(const RepArgs64 A) {
+    bh_pdl_trigger();
+    bh_pdl_wait();
+    rep_block64<D, COUNT, QUERY>(A, blockIdx.x, gridDim.x);
+}
+
+struct AttArgs64 {
+    const int64_t *__restrict__ rp;
+    const int32_t *__restrict__ col;
+    const double *__restrict__ val;
+    const double2 *__restrict__ y;
+    int64_t row_begin, row_end;
+    double exag_param;
+    const bh_sched_t *__restrict__ sched;
+    double2 *__restrict__ attr;
+};
+
+// Attractive sweep CTA `bid` of `nblk` (THREADS threads), G lanes per row
+// (forces.py:56-71 in f64).
+template <int G, bool PADDED, int THREADS>
+__device__ __forceinline__ void att_block64(const AttArgs64 &A, int64_t bid,
+                                            int64_t nblk) {
+    constexpr int kRows = THREADS / G;
+    const int64_t *__restrict__ rp = A.rp;
+    const int32_t *__restrict__ col = A.col;
+    const double *__restrict__ val = A.val;
+    const double2 *__restrict__ y = A.y;
+    const int64_t row_end = A.row_end;
+    const bh_sched_t *__restrict__ sched = A.sched;
     const double exag = sched ? (sched->iteration < sched->exaggeration_iters
                                      ? sched->exaggeration_f64
                                      : 1.0)
-                              : exag_param;
+                              : A.exag_param;
     const int gl = threadIdx.x % G;
-    for (int64_t r0 = row_begin + (int64_t)blockIdx.x * (256 / G); r0 < row_end;
-         r0 += (int64_t)gridDim.x * (256 / G)) {
+    for (int64_t r0 = A.row_begin + bid * kRows; r0 < row_end;
+         r0 += nblk * kRows) {
         const int64_t row = r0 + threadIdx.x / G;
         const bool ok = row < row_end;
         int64_t s = 0, e = 0;
@@ -200,8 +224,7 @@ k_attractive64(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
             yi = y[row];
         }
         double a0 = 0.0, a1 = 0.0;
-        auto term = [&](int32_t j, double v) {
-            const double2 yj = __ldg(&y[j]);
+        auto term = [&](const double2 yj, double v) {
             const double dx = __dsub_rn(yi.x, yj.x), dy = __dsub_rn(yi.y, yj.y);
             const double pq = __ddiv_rn(
                 __dmul_rn(v, exag),
@@ -214,21 +237,46 @@ k_attractive64(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                 const int4 c = ld_stream_i4(col + q);
                 const double2 v01 = ld_stream_d2(val + q);
                 const double2 v23 = ld_stream_d2(val + q + 2);
-                term(c.x, v01.x);
-                term(c.y, v01.y);
-                term(c.z, v23.x);
-                term(c.w, v23.y);
+                // all four gathers in flight before the arithmetic
+                const double2 y0 = __ldg(&y[c.x]), y1 = __ldg(&y[c.y]);
+                const double2 y2 = __ldg(&y[c.z]), y3 = __ldg(&y[c.w]);
+                term(y0, v01.x);
+                term(y1, v01.y);
+                term(y2, v23.x);
+                term(y3, v23.y);
             }
         } else {
-            for (int64_t q = s + gl; q < e; q += G) term(col[q], val[q]);
+            for (int64_t q = s + gl; q < e; q += G) term(__ldg(&y[col[q]]), val[q]);
         }
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) {
             a0 = __dadd_rn(a0, __shfl_xor_sync(0xffffffffu, a0, o));
             a1 = __dadd_rn(a1, __shfl_xor_sync(0xffffffffu, a1, o));
         }
-        if (ok && gl == 0) attr[row] = make_double2(a0, a1);
+        if (ok && gl == 0) A.attr[row] = make_double2(a0, a1);
     }
+}
+
+template <int G, bool PADDED>
+__global__ void __launch_bounds__(256) k_attractive64(const AttArgs64 A) {
+    bh_pdl_trigger();
+    bh_pdl_wait();
+    att_block64<G, PADDED, 256>(A, blockIdx.x, gridDim.x);
+}
+
+// The fused f64 force pass (the f32 k_forces, forces.cu): traversal and sweep
+// CTAs interleaved nr : na by block index.
+template <int D, int G, bool PADDED>
+__global__ void __launch_bounds__(kRepThreads)
+k_forces64(const RepArgs64 R, const AttArgs64 A, int64_t nr, int64_t na) {
+    bh_pdl_trigger();
+    bh_pdl_wait();
+    const int64_t b = blockIdx.x, nb = nr + na;
+    const int64_t before = (b * na) / nb, upto = ((b + 1) * na) / nb;
+    if (upto > before)
+        att_block64<G, PADDED, kRepThreads>(A, before, na);
+    else
+        rep_block64<D, false, false>(R, b - upto, nr);
 }
 
 // Exact O(N^2) repulsion in f64 (forces.py:153-173), tiles in shared memory.
@@ -306,7 +354,8 @@ extern "C" int bh_repulsive_f64(const bh_tree_t *t, const bh_bounds_t *bounds,
                       (const double2 *)y_query, bounds, t->status, theta,
                       t_begin, t_end, sorted_out, (double2 *)rep, zpart,
                       (int4 *)counts, zblock, ticket, z_out};
-#define BH_REP64(D, CNT, Q) k_repulsive64<D, CNT, Q><<<grid, kRepThreads, 0, st>>>(A)
+#define BH_REP64(D, CNT, Q)                                                   \
+    BH_LAUNCH("k_repulsive64", (k_repulsive64<D, CNT, Q>), grid, kRepThreads, 0, st, A)
 #define BH_REP64_2(D)                                                         \
     if (y_query) {                                                            \
         if (counts) BH_REP64(D, true, true); else BH_REP64(D, false, true);   \
@@ -322,7 +371,6 @@ extern "C" int bh_repulsive_f64(const bh_tree_t *t, const bh_bounds_t *bounds,
     }
 #undef BH_REP64
 #undef BH_REP64_2
-    BH_CHECK_LAUNCH("k_repulsive64");
     return BH_OK;
 }
 
@@ -338,15 +386,73 @@ extern "C" int bh_attractive_f64(const int64_t *row_ptr, const int32_t *col,
     constexpr int G = 16;
     const int grid = bh_blocks(row_end - row_begin, 256 / G);
     cudaStream_t st = bh_cs(stream);
+    const AttArgs64 A{row_ptr, col, val, (const double2 *)y, row_begin,
+                      row_end, exaggeration, sched, (double2 *)attr};
     if (padded)
-        k_attractive64<G, true><<<grid, 256, 0, st>>>(
-            row_ptr, col, val, (const double2 *)y, row_begin, row_end,
-            exaggeration, sched, (double2 *)attr);
+        BH_LAUNCH("k_attractive64", (k_attractive64<G, true>), grid, 256, 0, st, A);
     else
-        k_attractive64<G, false><<<grid, 256, 0, st>>>(
-            row_ptr, col, val, (const double2 *)y, row_begin, row_end,
-            exaggeration, sched, (double2 *)attr);
-    BH_CHECK_LAUNCH("k_attractive64");
+        BH_LAUNCH("k_attractive64", (k_attractive64<G, false>), grid, 256, 0, st, A);
+    return BH_OK;
+}
+
+extern "C" int bh_forces_f64(const bh_tree_t *t, const bh_bounds_t *bounds,
+                             double theta, int64_t t_begin, int64_t t_end,
+                             int sorted_out, double *rep, double *zblock,
+                             double *z_out, void *ws, size_t ws_bytes,
+                             const int64_t *row_ptr, const int32_t *col,
+                             const double *val, int64_t n_rows, int padded,
+                             const double *y, int64_t row_begin,
+                             int64_t row_end, double exaggeration,
+                             const bh_sched_t *sched, double *attr,
+                             bh_stream_t stream) {
+    BH_REQUIRE(theta >= 0, "theta must be >= 0, got %g", theta);
+    BH_REQUIRE(t->precision == 64, "bh_forces_f64 needs a precision-64 tree");
+    BH_REQUIRE(t_begin >= 0 && t_end <= t->n_points && t_begin <= t_end,
+               "bad point range");
+    BH_REQUIRE(row_begin >= 0 && row_end <= n_rows && row_begin <= row_end,
+               "bad row range");
+    if (t_end == t_begin || row_end == row_begin) {
+        int rc = bh_attractive_f64(row_ptr, col, val, n_rows, padded, y,
+                                   row_begin, row_end, exaggeration, sched,
+                                   attr, stream);
+        if (rc != BH_OK) return rc;
+        return bh_repulsive_f64(t, bounds, theta, nullptr, t_begin, t_end,
+                                sorted_out, rep, nullptr, zblock, z_out,
+                                nullptr, ws, ws_bytes, stream);
+    }
+    BH_REQUIRE(ws_bytes >= bh_repulsive_workspace_bytes(t_end - t_begin),
+               "repulsive workspace too small");
+    constexpr int G = 16;
+    const int64_t nr = rep_grid(t_end - t_begin);
+    const int64_t na = std::max<int64_t>(
+        1, std::min<int64_t>((nr + 1) / 2,
+                             bh_blocks(row_end - row_begin, kRepThreads / G)));
+    char *w = (char *)ws;
+    if (!zblock) zblock = (double *)w;
+    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(double) * nr));
+    const RepArgs64 R{(const void *)t->node, (const double2 *)t->ys, t->order,
+                      nullptr, bounds, t->status, theta, t_begin, t_end,
+                      sorted_out, (double2 *)rep, nullptr, nullptr, zblock,
+                      ticket, z_out};
+    const AttArgs64 A{row_ptr, col, val, (const double2 *)y, row_begin,
+                      row_end, exaggeration, sched, (double2 *)attr};
+    cudaStream_t st = bh_cs(stream);
+    const unsigned grid = (unsigned)(nr + na);
+#define BH_FORCES64(D)                                                        \
+    if (padded)                                                               \
+        BH_LAUNCH("k_forces64", (k_forces64<D, G, true>), grid, kRepThreads,  \
+                  0, st, R, A, nr, na);                                       \
+    else                                                                      \
+        BH_LAUNCH("k_forces64", (k_forces64<D, G, false>), grid, kRepThreads, \
+                  0, st, R, A, nr, na);
+    if (t->code_bits == 32) {
+        BH_FORCES64(16)
+    } else if (t->code_bits == 64) {
+        BH_FORCES64(32)
+    } else {
+        return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
+    }
+#undef BH_FORCES64
     return BH_OK;
 }
 

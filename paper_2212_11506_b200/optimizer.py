@@ -220,7 +220,7 @@ class Engine:
 
     def _fused(self, timed: bool) -> bool:
         return (self.shard is None and self.fuse and not self.overlap
-                and not self.f64 and (not timed or self.fuse_timed))
+                and (not timed or self.fuse_timed))
 
     def fn(self, name: str) -> str:
         """Library entry point in the run precision."""
@@ -391,7 +391,7 @@ class Engine:
         if self._fused(ev is not None):
             # both force passes in one launch, their CTAs sharing the SMs
             # (bitwise the same results as the two kernels)
-            call("bh_forces", t.sref(), ptr(self.bounds), self.theta, 0, n, 0,
+            call(self.fn("bh_forces"), t.sref(), ptr(self.bounds), self.theta, 0, n, 0,
                  ptr(self.rep), None, ptr(self.z_dev), ptr(self.ws_rep),
                  self.ws_rep.numel(), ptr(self.rp), ptr(self.col),
                  ptr(self.val), n, 1, ptr(y), 0, n, 1.0, ptr(self.sched),

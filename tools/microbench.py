@@ -43,12 +43,18 @@ def child(args):
         eng = bh.Engine(p, e, cfg)
         eng.run(args.preroll)
         np.save(cache, e.y.cpu().numpy())
+    if args.precision == "f64":  # the same state in the f64 run precision
+        p = bh.from_csr(prob["row_offsets"], prob["col"],
+                        prob["val"].astype(np.float64))
+        e = bh.embedding_from(e.y.cpu().numpy().astype(np.float64))
+        cfg = bh.TsneConfig(theta=args.theta, precision="f64")
     eng = bh.Engine(p, e, cfg)
+    fn = eng.fn
     t = eng.tree
     st = stream()
 
     def build():
-        call("bh_morton", ptr(eng.y), eng.n, ptr(eng.bounds), 32, 0,
+        call(fn("bh_morton"), ptr(eng.y), eng.n, ptr(eng.bounds), 32, 0,
              ptr(eng.codes), st)
         call("bh_sort", ptr(eng.codes), eng.n, 32, ptr(t.sorted_codes),
              ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st)
@@ -75,12 +81,12 @@ def child(args):
         b.synchronize()
         return a.elapsed_time(b) / reps
 
-    att = lambda: call("bh_attractive", ptr(eng.rp), ptr(eng.col), ptr(eng.val),
+    att = lambda: call(fn("bh_attractive"), ptr(eng.rp), ptr(eng.col), ptr(eng.val),
                        eng.n, 1, ptr(eng.y), 0, eng.n, 1.0, None, ptr(eng.attr), st)
-    rep = lambda: call("bh_repulsive", t.sref(), ptr(eng.bounds), float(args.theta),
+    rep = lambda: call(fn("bh_repulsive"), t.sref(), ptr(eng.bounds), float(args.theta),
                        None, 0, eng.n, 0, ptr(eng.rep), None, None, ptr(eng.z_dev),
                        None, ptr(eng.ws_rep), eng.ws_rep.numel(), st)
-    fused = lambda: call("bh_forces", t.sref(), ptr(eng.bounds), float(args.theta),
+    fused = lambda: call(fn("bh_forces"), t.sref(), ptr(eng.bounds), float(args.theta),
                          0, eng.n, 0, ptr(eng.rep), None, ptr(eng.z_dev),
                          ptr(eng.ws_rep), eng.ws_rep.numel(), ptr(eng.rp),
                          ptr(eng.col), ptr(eng.val), eng.n, 1, ptr(eng.y), 0,
@@ -92,7 +98,7 @@ def child(args):
         t.build(eng.y)
 
     out = {"knobs": {k: v for k, v in os.environ.items() if k.startswith("BH_")},
-           "iteration": args.preroll,
+           "iteration": args.preroll, "precision": args.precision,
            "attractive_ms": timeit(att, args.reps),
            "repulsive_ms": timeit(rep, args.reps),
            "forces_fused_ms": timeit(fused, args.reps),
@@ -108,6 +114,7 @@ def main():
     ap.add_argument("--theta", type=float, default=0.5)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--precision", choices=["f32", "f64"], default="f32")
     ap.add_argument("--sweep", nargs="*", default=[],
                     help="NAME=v1,v2,... environment knobs to sweep")
     args = ap.parse_args()
@@ -121,7 +128,7 @@ def main():
         env = dict(os.environ, **c)
         cmd = [sys.executable, __file__, "--child", "--config", args.config,
                "--preroll", str(args.preroll), "--theta", str(args.theta),
-               "--reps", str(args.reps)]
+               "--reps", str(args.reps), "--precision", args.precision]
         subprocess.run(cmd, env=env, check=False)
 
 
