@@ -20,7 +20,7 @@ using Rec64 = NodeRec<double>;
 
 __device__ __forceinline__ void leaf_pair64(double2 yi, double2 p, Acc64 &a) {
     const double dx = __dsub_rn(yi.x, p.x), dy = __dsub_rn(yi.y, p.y);
-    const double k = __ddiv_rn(1.0, __dadd_rn(__dadd_rn(1.0, __dmul_rn(dx, dx)),
+    const double k = __drcp_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(dx, dx)),
                                              __dmul_rn(dy, dy)));
     a.z = __dadd_rn(a.z, k);
     const double k2 = __dmul_rn(k, k);
@@ -74,7 +74,7 @@ __device__ __forceinline__ uint32_t bh_child64(const Ctx64 &g, double2 c,
         cn.accepted += acc;
     }
     if (g.mine && acc) {
-        const double k = __ddiv_rn(1.0, __dadd_rn(1.0, d2));
+        const double k = __drcp_rn(__dadd_rn(1.0, d2));
         const double mk = __dmul_rn((double)m, k);
         a.z = __dadd_rn(a.z, mk);
         const double mk2 = __dmul_rn(mk, k);
