@@ -306,6 +306,8 @@ def ours_arm(args, rank, world):
     eng.overlap = args.overlap
     eng.fuse = not args.no_fuse
     eng.chunk_graph = args.chunk_graph
+    if args.attr_split is not None:
+        eng.attr_split = args.attr_split
     eng.prepare(timings=True)  # every CUDA graph captured before timing
     if args.preroll:
         eng.run(args.preroll)
@@ -409,6 +411,7 @@ def ours_arm(args, rank, world):
     e2e = dict(runs[0], value=vals[len(vals) // 2],
                repeats=[r["value"] for r in runs],
                breakdowns=[r["breakdown_s"] for r in runs],
+               clocks_per_run=[r["clocks"] for r in runs],
                summary=f"median of {len(runs)} end-to-end runs")
     e2e["per_step_host_state"] = e2e_host(bh, p, cfg, y_end, args)
 
@@ -448,22 +451,26 @@ def e2e_run(bh, prob, cfg, args):
     ro, co, va = pin(prob["row_offsets"]), pin(prob["col"]), pin(prob["val"])
     y0 = pin(prob["y0"])
     iters = args.warmup + args.steps
+    # release the previous run's engine before timing this one
+    import gc
+    gc.collect()
     torch.cuda.synchronize()
     tick = time.perf_counter
-    t0 = tick()
-    p = bh.from_csr(ro, co, va)
-    e = bh.embedding_from(y0)
-    torch.cuda.synchronize()
-    t1 = tick()
-    eng = bh.Engine(p, e, cfg)
-    torch.cuda.synchronize()
-    t2 = tick()
-    eng.run(iters)
-    torch.cuda.synchronize()
-    t3 = tick()
-    y_out = e.y.cpu()
-    torch.cuda.synchronize()
-    dt = tick() - t0
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+        t0 = tick()
+        p = bh.from_csr(ro, co, va)
+        e = bh.embedding_from(y0)
+        torch.cuda.synchronize()
+        t1 = tick()
+        eng = bh.Engine(p, e, cfg)
+        torch.cuda.synchronize()
+        t2 = tick()
+        eng.run(iters)
+        torch.cuda.synchronize()
+        t3 = tick()
+        y_out = e.y.cpu()
+        torch.cuda.synchronize()
+        dt = tick() - t0
     h2d = sum(int(t.numel() * t.element_size()) for t in (ro, co, va, y0))
     d2h = int(y_out.numel() * y_out.element_size())
     return {"value": iters / dt, "unit": "it/s",
@@ -473,7 +480,8 @@ def e2e_run(bh, prob, cfg, args):
                    "upload, CSR padding, CUDA-graph capture and readback",
             "steps": iters,
             "breakdown_s": {"upload": t1 - t0, "engine_init": t2 - t1,
-                            "run": t3 - t2, "readback": t0 + dt - t3}}
+                            "run": t3 - t2, "readback": t0 + dt - t3},
+            "clocks": clk.summary()}
 
 
 def e2e_host(bh, p, cfg, y_host, args):
@@ -655,6 +663,8 @@ def main():
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--relabel-every", type=int, default=50,
                     help="Morton relabeling period of the engine (0: never)")
+    ap.add_argument("--attr-split", type=float, default=None,
+                    help="fraction of CSR rows swept under the tree build")
     ap.add_argument("--chunk-graph", action="store_true",
                     help="replay one graph per graph_chunk iterations (A/B)")
     ap.add_argument("--no-fuse", action="store_true",

@@ -299,6 +299,11 @@ class Engine:
         # (measured +0.6% at C3, profiles/README.md); off by default so the
         # cooperative summarize launch never contends for SM slots
         self.overlap = False
+        # fraction of the CSR rows swept on the (low-priority) side stream
+        # under the latency-bound tree build in the fused fast path; the rest
+        # run inside the fused force launch.  Measured at C3 (it/s): 0: 487,
+        # 0.3: 498, 0.4: 505, 0.45: 506, 0.6: 499, 1.0: 479
+        self.attr_split = 0.45
         # fuse: the untimed fast path launches the fused force pass
         # (bh_forces); the evented (StepTimings) path keeps the two kernels
         # apart for the per-stage breakdown unless fuse_timed is set
@@ -359,6 +364,19 @@ class Engine:
              ptr(self.codes), st)
         side = (self.shard is not None and self.shard_overlap
                 and ev is None)
+        # fused fast path: the first `split` CSR rows are swept on the side
+        # stream under the latency-bound tree build (they need only Y and P),
+        # the rest inside the fused force launch
+        split = (int(self.n * self.attr_split)
+                 if self._fused(ev is not None) and ev is None else 0)
+        if split > 0:
+            self.fork_ev.record(torch.cuda.current_stream())
+            with torch.cuda.stream(self.side):
+                self.side.wait_event(self.fork_ev)
+                call(self.fn("bh_attractive"), ptr(self.rp), ptr(self.col),
+                     ptr(self.val), n, 1, ptr(y), 0, split, 1.0,
+                     ptr(self.sched), ptr(self.attr), stream())
+                self.join_ev.record(self.side)
         if side:
             # sharded fast path: this rank's attractive rows and their
             # all-gather run on the side stream under the replicated tree
@@ -394,8 +412,10 @@ class Engine:
             call(self.fn("bh_forces"), t.sref(), ptr(self.bounds), self.theta, 0, n, 0,
                  ptr(self.rep), None, ptr(self.z_dev), ptr(self.ws_rep),
                  self.ws_rep.numel(), ptr(self.rp), ptr(self.col),
-                 ptr(self.val), n, 1, ptr(y), 0, n, 1.0, ptr(self.sched),
+                 ptr(self.val), n, 1, ptr(y), split, n, 1.0, ptr(self.sched),
                  ptr(self.attr), st)
+            if split > 0:
+                torch.cuda.current_stream().wait_event(self.join_ev)
             rec(4)
             rec(5)
             rep, rep_rank = self.rep, None
@@ -445,7 +465,7 @@ class Engine:
         """One iteration without timing events (the fast path: replayed
         back to back, the host only syncs at chunk boundaries)."""
         key = ("fast", self.csr_key, self.overlap, self._fused(False),
-               self.shard_overlap)
+               self.shard_overlap, self.attr_split)
         if key not in self.graphs:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.main):
@@ -458,7 +478,7 @@ class Engine:
         graph launch per chunk instead of one per iteration."""
         k = self.cfg.graph_chunk
         key = ("fastk", k, self.csr_key, self.overlap, self._fused(False),
-               self.shard_overlap)
+               self.shard_overlap, self.attr_split)
         if key not in self.graphs:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.main):
