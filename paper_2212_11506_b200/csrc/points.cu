@@ -14,7 +14,10 @@
 namespace bh {
 
 constexpr int kPtThreads = 256;
-constexpr int kPtMaxBlocks = kSMs * 8;
+#ifndef BH_PT_BLOCKS_PER_SM
+#define BH_PT_BLOCKS_PER_SM 4  // update 26 us vs 28 (8), 34 (16)
+#endif
+constexpr int kPtMaxBlocks = kSMs * BH_PT_BLOCKS_PER_SM;
 
 __device__ __forceinline__ uint32_t spread16(uint32_t x) {
     x &= 0xFFFFu;
