@@ -658,7 +658,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=25)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=50)
-    ap.add_argument("--e2e-repeats", type=int, default=3,
+    ap.add_argument("--e2e-repeats", type=int, default=5,
                     help="end-to-end runs through the public API (median)")
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--relabel-every", type=int, default=50,
