@@ -217,10 +217,17 @@ class Engine:
 
     STAGE_EVENTS_FUSED = {"tree": (0, 1), "summarize": (1, 2),
                           "forces": (2, 4), "update": (5, 6)}
+    # with the split sweep: "attractive" = the side-stream launch (concurrent
+    # with the tree build), "forces" = end of summarize to the join
+    STAGE_EVENTS_FUSED_SPLIT = dict(STAGE_EVENTS_FUSED, attractive=(7, 3))
 
     def _fused(self, timed: bool) -> bool:
         return (self.shard is None and self.fuse and not self.overlap
                 and (not timed or self.fuse_timed))
+
+    def split_rows(self) -> int:
+        """CSR rows [0, split) swept on the side stream in the fused path."""
+        return int(self.n * self.attr_split)
 
     def fn(self, name: str) -> str:
         """Library entry point in the run precision."""
@@ -230,7 +237,8 @@ class Engine:
         if self.shard is not None:
             return self.STAGE_EVENTS_SHARDED
         if self._fused(True):
-            return self.STAGE_EVENTS_FUSED
+            return (self.STAGE_EVENTS_FUSED_SPLIT if self.split_rows()
+                    else self.STAGE_EVENTS_FUSED)
         return self.STAGE_EVENTS if self.overlap else self.STAGE_EVENTS_SEQ
 
     def __init__(self, p: SparseAffinity, e: Embedding, cfg: TsneConfig,
@@ -367,15 +375,16 @@ class Engine:
         # fused fast path: the first `split` CSR rows are swept on the side
         # stream under the latency-bound tree build (they need only Y and P),
         # the rest inside the fused force launch
-        split = (int(self.n * self.attr_split)
-                 if self._fused(ev is not None) and ev is None else 0)
+        split = self.split_rows() if self._fused(ev is not None) else 0
         if split > 0:
             self.fork_ev.record(torch.cuda.current_stream())
             with torch.cuda.stream(self.side):
                 self.side.wait_event(self.fork_ev)
+                rec(7)
                 call(self.fn("bh_attractive"), ptr(self.rp), ptr(self.col),
                      ptr(self.val), n, 1, ptr(y), 0, split, 1.0,
                      ptr(self.sched), ptr(self.attr), stream())
+                rec(3)
                 self.join_ev.record(self.side)
         if side:
             # sharded fast path: this rank's attractive rows and their
@@ -465,7 +474,8 @@ class Engine:
                  for _ in range(self.N_EVENTS)] for _ in range(k)]
 
     def _graph(self, k):
-        key = (k, self.csr_key, self.overlap, self._fused(True))
+        key = (k, self.csr_key, self.overlap, self._fused(True),
+               self.attr_split)
         if key not in self.graphs:
             evs = self._events(k)
             g = self._capture(lambda: [self._enqueue(evs[i]) for i in range(k)])
