@@ -349,12 +349,21 @@ __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
     }
 }
 
+#ifndef BH_ATTR_THREADS
+#define BH_ATTR_THREADS 256
+#endif
+#ifndef BH_ATTR_MINB
+#define BH_ATTR_MINB 8  // 32 registers: 0.518 ms vs 0.612 uncapped (C3 it. 600)
+#endif
+constexpr int kAttThreads = BH_ATTR_THREADS;
+
 template <int G, bool PADDED>
-__global__ void __launch_bounds__(256) k_attractive(const AttArgs A) {
+__global__ void __launch_bounds__(kAttThreads, BH_ATTR_MINB)
+k_attractive(const AttArgs A) {
     bh_pdl_trigger();  // the successor may launch early (PDL)
     bh_pdl_wait();     // the predecessor's results are visible
 
-    att_block<G, PADDED, 256>(A, blockIdx.x, gridDim.x);
+    att_block<G, PADDED, kAttThreads>(A, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -568,13 +577,13 @@ extern "C" int bh_attractive(const int64_t *row_ptr, const int32_t *col,
                     exaggeration, sched, (float2 *)attr};
 #define BH_ATTR(G)                                                            \
     {                                                                         \
-        const int grid = bh_blocks(row_end - row_begin, 256 / G);             \
+        const int grid = bh_blocks(row_end - row_begin, kAttThreads / G);     \
         if (padded)                                                           \
-            BH_LAUNCH("k_attractive", (k_attractive<G, true>), grid, 256, 0,  \
-                      st, A);                                                 \
+            BH_LAUNCH("k_attractive", (k_attractive<G, true>), grid,          \
+                      kAttThreads, 0, st, A);                                 \
         else                                                                  \
-            BH_LAUNCH("k_attractive", (k_attractive<G, false>), grid, 256, 0, \
-                      st, A);                                                 \
+            BH_LAUNCH("k_attractive", (k_attractive<G, false>), grid,         \
+                      kAttThreads, 0, st, A);                                 \
     }
     switch (g_env) {
         case 4: BH_ATTR(4) break;
