@@ -422,6 +422,9 @@ def ours_arm(args, rank, world):
             "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
             "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
             "peak_source": peak_src,
+            # the north star's nominal ~8 TB/s, for reference
+            "peak_nominal": 8000.0,
+            "frac_nominal": kernels[dom]["achieved_gbs"] / 8000.0,
             "visits_per_point": (cnt[0] + cnt[1]) / n,
             "leaf_points_per_point": cnt[2] / n}
 
