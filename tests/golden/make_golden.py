@@ -233,6 +233,22 @@ def full_run_c0():
     print("c0 kl", kl, timings.kl_history)
 
 
+def full_run_c1():
+    """C1 (BASELINE.json configs[1], N=70k, D=50) full 1000-iteration f32
+    run of the reference: its KL and periodic KL (the final-KL parity at a
+    larger size; the kNN graph is recomputed from the data on the GPU)."""
+    import bhtsne
+    sys.path.insert(0, REPO)
+    from paper_2212_11506_b200.workloads import c1
+    x = c1()
+    cfg = bhtsne.TsneConfig(precision="f32", seed=0, kl_every=250, threads=8)
+    e, timings, kl = bhtsne.run(bhtsne.InputMatrix(x), cfg)
+    np.savez_compressed(os.path.join(HERE, "c1_run.npz"), kl=np.array(kl),
+                        kl_history=np.array(timings.kl_history),
+                        n=np.array(x.shape[0]))
+    print("c1 kl", kl, timings.kl_history)
+
+
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "--child":
         sys.path.insert(0, REF_SRC)
@@ -247,6 +263,8 @@ def main():
             affinity_f64()
         elif what == "c0":
             full_run_c0()
+        elif what == "c1":
+            full_run_c1()
         return
     jobs = sys.argv[1:] or ["trees64", "trees32", "affinity", "affinity_f64",
                             "c0"]

@@ -384,6 +384,23 @@ def test_c0_full_run_kl_within_1pct(bh):
     np.testing.assert_array_equal(e2.y.cpu().numpy(), e.y.cpu().numpy())
 
 
+@pytest.mark.slow
+def test_c1_full_run_kl_within_1pct(bh):
+    """C1 (N=70k, D=50): the whole pipeline from raw data on the GPU (exact
+    kNN, BSP, P, Y0, 1000 iterations, exact KL) against the unmodified
+    reference's run() on the same data (tests/golden c1_run)."""
+    from paper_2212_11506_b200.workloads import c1
+    g = golden("c1_run")
+    e, timings, kl = bh.run(c1(), bh.TsneConfig(kl_every=250))
+    ref = float(g["kl"])
+    assert abs(kl - ref) / ref < 0.01, (kl, ref)
+    ours = [k for _, k in timings.kl_history]
+    theirs = [float(k) for _, k in g["kl_history"]]
+    assert len(ours) == len(theirs) == 4
+    # the periodic BH-KL follows the same descent
+    assert all(abs(a - b) / b < 0.05 for a, b in zip(ours, theirs)), (ours, theirs)
+
+
 def test_estimator_fit_transform(bh):
     from paper_2212_11506_b200.workloads import c0
     est = bh.BarnesHutTSNE(n_iter=300, exaggeration_iters=100)
