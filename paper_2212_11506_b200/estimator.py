@@ -15,7 +15,7 @@ import hashlib
 import numpy as np
 
 from . import __version__
-from .optimizer import STAGES, TsneConfig, run
+from .optimizer import REPORT_STAGES, TsneConfig, run
 
 
 class BarnesHutTSNE:
@@ -85,7 +85,7 @@ class BarnesHutTSNE:
             "seed": cfg.seed,
             "precision": cfg.precision,
             "wall_s": timings.total_wall_s,
-            "stage_totals_s": {s: timings.total(s) for s in STAGES},
+            "stage_totals_s": {s: timings.total(s) for s in REPORT_STAGES},
             "kl": kl,
             "kl_history": timings.kl_history,
         }

@@ -43,6 +43,8 @@ from .quadtree import (DEFAULT_CODE_BITS, TreeArrays, as_points, build_tree,
 
 STAGES = ("knn", "bsp", "tree", "summarize", "attractive", "repulsive",
           "update")
+# the stages a report lists: the reference's, plus the fused force launch
+REPORT_STAGES = STAGES + ("forces",)
 # "forces": the fused attractive + repulsive launch (Engine.fuse_timed)
 EXTRA_STAGES = ("comm", "relabel", "forces")
 MOMENTUM_SWITCH_ITER = 250
@@ -764,6 +766,11 @@ def run(x, cfg: TsneConfig, *, knn=None) -> tuple:
     p, _ = affinities(x, cfg, knn=knn, timings=timings)
     e = init_embedding(n, cfg.seed, dtype=cfg.dtype)
     eng = Engine(p, e, cfg, schedule=True)
+    # the fast pipeline (side sweep + fused force launch), evented: the
+    # timings carry "forces" (the fused launch, end of summarize to the join)
+    # and "attractive" (the side-stream sweep, concurrent with the tree build)
+    # instead of separate attractive / repulsive kernels
+    eng.fuse_timed = True
     kl_history = []
     done = 0
     while done < cfg.n_iter:

@@ -249,6 +249,21 @@ def full_run_c1():
     print("c1 kl", kl, timings.kl_history)
 
 
+def full_run_c2():
+    """C2 (BASELINE.json configs[2], N=250k) full f32 run of the reference."""
+    import bhtsne
+    sys.path.insert(0, REPO)
+    from paper_2212_11506_b200.workloads import c2
+    x = c2()
+    cfg = bhtsne.TsneConfig(precision="f32", seed=0, kl_every=250, threads=8)
+    e, timings, kl = bhtsne.run(bhtsne.InputMatrix(x), cfg)
+    np.savez_compressed(os.path.join(HERE, "c2_run.npz"), kl=np.array(kl),
+                        kl_history=np.array(timings.kl_history),
+                        n=np.array(x.shape[0]),
+                        wall_s=np.array(timings.total_wall_s))
+    print("c2 kl", kl, timings.kl_history, timings.total_wall_s)
+
+
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "--child":
         sys.path.insert(0, REF_SRC)
@@ -265,6 +280,8 @@ def main():
             full_run_c0()
         elif what == "c1":
             full_run_c1()
+        elif what == "c2":
+            full_run_c2()
         return
     jobs = sys.argv[1:] or ["trees64", "trees32", "affinity", "affinity_f64",
                             "c0"]

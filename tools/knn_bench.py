@@ -1,0 +1,22 @@
+"""Exact GPU kNN timing (tuning aid): python tools/knn_bench.py c1 c2 ..."""
+import json
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2212_11506_b200 import workloads  # noqa: E402
+from paper_2212_11506_b200.knn import knn_exact  # noqa: E402
+
+for name in sys.argv[1:] or ["c1"]:
+    x = getattr(workloads, name)()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    g = knn_exact(x, 90)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    n = x.shape[0]
+    print(json.dumps({"config": name, "n": n, "d": x.shape[1], "k": 90,
+                      "seconds": dt, "pairs_per_s": n * (n - 1) / dt}),
+          flush=True)
