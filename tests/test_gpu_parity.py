@@ -401,6 +401,29 @@ def test_c1_full_run_kl_within_1pct(bh):
     assert all(abs(a - b) / b < 0.05 for a, b in zip(ours, theirs)), (ours, theirs)
 
 
+@pytest.mark.parametrize("n", [3, 5, 17, 33, 129, 300])
+def test_small_sizes_through_run(bh, n):
+    """Ragged sizes (partial warps / CTAs, fewer rows than one sweep batch,
+    side-sweep split of 0 or 1 rows) through the whole public pipeline,
+    against the same run with separate force kernels."""
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, 4)).astype(np.float32)
+    cfg = bh.TsneConfig(perplexity=min(30.0, (n - 1) / 3.0 + 0.5), n_iter=60,
+                        exaggeration_iters=20, relabel_every=7, graph_chunk=5)
+    e, timings, kl = bh.run(x, cfg)
+    y = e.y.cpu().numpy()
+    assert y.shape == (n, 2) and np.isfinite(y).all() and np.isfinite(kl)
+    assert timings.calls("tree") == 60
+    # the engine's separate-kernel path gives the bitwise same trajectory
+    from paper_2212_11506_b200.optimizer import affinities
+    p, _ = affinities(x, cfg)
+    e2 = bh.init_embedding(n, cfg.seed)
+    eng = bh.Engine(p, e2, cfg)
+    eng.fuse = False
+    eng.run(60)
+    np.testing.assert_array_equal(e2.y.cpu().numpy(), y)
+
+
 def test_estimator_fit_transform(bh):
     from paper_2212_11506_b200.workloads import c0
     est = bh.BarnesHutTSNE(n_iter=300, exaggeration_iters=100)
