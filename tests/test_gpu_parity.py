@@ -401,6 +401,20 @@ def test_c1_full_run_kl_within_1pct(bh):
     assert all(abs(a - b) / b < 0.05 for a, b in zip(ours, theirs)), (ours, theirs)
 
 
+@pytest.mark.slow
+def test_c2_full_run_kl_within_1pct(bh):
+    """C2 (N=250k, D=50, 20 rotated anisotropic clusters): the whole GPU
+    pipeline from raw data against the unmodified reference's run()."""
+    from paper_2212_11506_b200.workloads import c2
+    g = golden("c2_run")
+    e, timings, kl = bh.run(c2(), bh.TsneConfig(kl_every=250))
+    ref = float(g["kl"])
+    assert abs(kl - ref) / ref < 0.01, (kl, ref)
+    ours = [k for _, k in timings.kl_history]
+    theirs = [float(k) for _, k in g["kl_history"]]
+    assert all(abs(a - b) / b < 0.05 for a, b in zip(ours, theirs)), (ours, theirs)
+
+
 @pytest.mark.parametrize("n", [3, 5, 17, 33, 129, 300])
 def test_small_sizes_through_run(bh, n):
     """Ragged sizes (partial warps / CTAs, fewer rows than one sweep batch,
