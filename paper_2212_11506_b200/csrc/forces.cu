@@ -34,6 +34,7 @@ struct GroupCtx {
     bool mine;
     uint32_t self;
     int lane;
+    uint32_t depth;  // of the group's children
 };
 
 // One child for one lane (the reference rule, forces.py:99-128).  Returns
@@ -102,10 +103,54 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
     return need;
 }
 
+#ifndef BH_REP_FAST
+// 1: groups above the deepest level (no coincident-code buckets there) use
+// bh_child_fast, one branch-free body per child; 0: bh_child everywhere
+#define BH_REP_FAST 1
+#endif
+
+// bh_child for a group whose children are above depth D, where every leaf
+// holds exactly one point (leaf iff count == 1 or depth == D,
+// quadtree.py:262-300).  Leaf vs internal is folded into the predicates: a
+// leaf is never approximated and its record is its point with mass 1, so
+// it "accepts" unconditionally (minus self, compared by the whole info
+// word); an internal node accepts iff d2 > R2.  Same decisions and
+// contributions as bh_child.
+template <bool COUNT>
+__device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
+                                                  const float4 r, float &fz,
+                                                  float &fx, float &fy,
+                                                  RepCounts &cn) {
+    const uint32_t info = __float_as_uint(r.w);
+    const uint32_t m = __float_as_uint(r.z);
+    const float dx = g.yi.x - r.x, dy = g.yi.y - r.y;
+    const float d2 = fmaf(dx, dx, dy * dy);
+    const bool leaf = (int32_t)info < 0;
+    const bool acc = leaf || d2 > g.r2;
+    if (COUNT && g.mine) {
+        if (leaf) {
+            cn.leafnodes++;
+            cn.leafpts += (int)m;
+        } else {
+            cn.internal++;
+            cn.accepted += acc;
+        }
+    }
+    const bool use = g.mine && acc && info != (BH_LEAF_BIT | g.self);
+    const float w = use ? __uint2float_rn(m) : 0.f;
+    const uint32_t need = ballot_full(g.mine && !acc);
+    const float k = rcp_approx(1.0f + d2);
+    const float wk = w * k, wk2 = wk * k;
+    fz += wk;
+    fx = fmaf(wk2, dx, fx);
+    fy = fmaf(wk2, dy, fy);
+    return need;
+}
+
 // Visit the CNT consecutive children starting at `first`, then push every
 // child some lane must open in one lane-parallel step (lane c writes child
 // c's entry; child 0 ends on top so the first subtree is popped first).
-template <int CNT, bool COUNT>
+template <int CNT, bool COUNT, bool FAST>
 __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
                                          Acc64 &a64, RepCounts &cn,
                                          uint4 *stk, int &sp) {
@@ -117,7 +162,8 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
 #pragma unroll
     for (int c = 0; c < CNT; c++) {
         inf[c] = __float_as_uint(rec[c].w);
-        pm[c] = bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
+        pm[c] = FAST ? bh_child_fast<COUNT>(g, rec[c], fz, fx, fy, cn)
+                     : bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
     }
     a64.z += (double)fz;
     a64.r0 += (double)fx;
@@ -135,7 +181,8 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
                     msk = pm[c];
                 }
             stk[sp + __popc(nz >> (g.lane + 1))] =
-                make_uint4(info, msk, __float_as_uint(g.r2 * 0.25f), 0u);
+                make_uint4(info, msk, __float_as_uint(g.r2 * 0.25f),
+                           g.depth + 1u);
         }
         sp += __popc(nz);
     }
@@ -144,7 +191,7 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
 // Stack entry (16 B, one STS.128 / broadcast LDS.128): x = the opened
 // node's info word (first child | (children - 1) << 29), y = mask of the
 // lanes that opened it, z = R2 = side^2 / theta^2 of the children's cells
-// (f32; exact quartering per level), w unused.
+// (f32; exact quartering per level), w = the depth of those children.
 struct RepArgs {
     const float4 *__restrict__ node;
     const float2 *__restrict__ ys;
@@ -219,14 +266,24 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const bool mine = (ent.y >> lane) & 1u;
         const float r2 = __uint_as_float(ent.z);
-        const GroupCtx g{node, ys, yi, r2, mine, self, lane};
+        const GroupCtx g{node, ys, yi, r2, mine, self, lane, ent.w};
         Acc64 a{z, r0, r1};
-        // straight-line code for the (warp-uniform) number of children
-        switch (cnt) {
-            case 1: bh_group<1, COUNT>(g, first, a, cn, stk, sp); break;
-            case 2: bh_group<2, COUNT>(g, first, a, cn, stk, sp); break;
-            case 3: bh_group<3, COUNT>(g, first, a, cn, stk, sp); break;
-            default: bh_group<4, COUNT>(g, first, a, cn, stk, sp); break;
+        // straight-line code for the (warp-uniform) number of children;
+        // the branch-free body above the deepest level (warp-uniform)
+        if (BH_REP_FAST && ent.w < (uint32_t)D) {
+            switch (cnt) {
+                case 1: bh_group<1, COUNT, true>(g, first, a, cn, stk, sp); break;
+                case 2: bh_group<2, COUNT, true>(g, first, a, cn, stk, sp); break;
+                case 3: bh_group<3, COUNT, true>(g, first, a, cn, stk, sp); break;
+                default: bh_group<4, COUNT, true>(g, first, a, cn, stk, sp); break;
+            }
+        } else {
+            switch (cnt) {
+                case 1: bh_group<1, COUNT, false>(g, first, a, cn, stk, sp); break;
+                case 2: bh_group<2, COUNT, false>(g, first, a, cn, stk, sp); break;
+                case 3: bh_group<3, COUNT, false>(g, first, a, cn, stk, sp); break;
+                default: bh_group<4, COUNT, false>(g, first, a, cn, stk, sp); break;
+            }
         }
         z = a.z;
         r0 = a.r0;
