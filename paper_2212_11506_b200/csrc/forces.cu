@@ -2,6 +2,7 @@
 // sweep (forces.py:56-82), exact O(N^2) repulsion (forces.py:153-182) and
 // the KL rows (optimizer.py:227-239).
 #include <algorithm>
+#include <type_traits>
 
 #include "forces.cuh"
 
@@ -116,7 +117,7 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
 // it "accepts" unconditionally (minus self, compared by the whole info
 // word); an internal node accepts iff d2 > R2.  Same decisions and
 // contributions as bh_child.
-template <bool COUNT>
+template <bool COUNT, bool SC>
 __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
                                                   const float4 r, float &fz,
                                                   float &fx, float &fy,
@@ -136,7 +137,10 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
             cn.accepted += acc;
         }
     }
-    const bool use = g.mine && acc && info != (BH_LEAF_BIT | g.self);
+    // lanes outside the mask are zeroed once per group (bh_group); with SC
+    // the self leaf is not tested here: it adds exactly k = 1/(1+0) = 1 to
+    // z and 0 to the force, and rep_block subtracts that 1 (SelfCorr)
+    const bool use = acc && (SC || info != (BH_LEAF_BIT | g.self));
     const float w = use ? __uint2float_rn(m) : 0.f;
     const uint32_t need = ballot_full(g.mine && !acc);
     const float k = rcp_approx(1.0f + d2);
@@ -150,7 +154,7 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
 // Visit the CNT consecutive children starting at `first`, then push every
 // child some lane must open in one lane-parallel step (lane c writes child
 // c's entry; child 0 ends on top so the first subtree is popped first).
-template <int CNT, bool COUNT, bool FAST>
+template <int CNT, bool COUNT, bool FAST, bool SC>
 __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
                                          Acc64 &a64, RepCounts &cn,
                                          uint4 *stk, int &sp) {
@@ -162,9 +166,10 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
 #pragma unroll
     for (int c = 0; c < CNT; c++) {
         inf[c] = __float_as_uint(rec[c].w);
-        pm[c] = FAST ? bh_child_fast<COUNT>(g, rec[c], fz, fx, fy, cn)
+        pm[c] = FAST ? bh_child_fast<COUNT, SC>(g, rec[c], fz, fx, fy, cn)
                      : bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
     }
+    if (FAST && !g.mine) fz = fx = fy = 0.f;  // exact: nothing of this group
     a64.z += (double)fz;
     a64.r0 += (double)fx;
     a64.r1 += (double)fy;
@@ -208,7 +213,38 @@ struct RepArgs {
     double *__restrict__ zblock;
     unsigned *__restrict__ ticket;
     double *__restrict__ z_out;
+    const void *__restrict__ codes;  // sorted codes (self correction)
+    int64_t n_points;
 };
+
+// Self correction (SC): when theta <= kScTheta no point accepts an
+// ancestor of its own leaf -- d^2 <= (2 sqrt2 r)^2 = 8 r^2 for the point and
+// the centre of mass inside one cell, while acceptance needs d^2 >
+// 4 r^2 / theta^2 >= 8.16 r^2 -- so every point whose leaf lies above depth
+// D (a single-point leaf, visited by the branch-free body) meets it exactly
+// once and its +1 is subtracted at the end.  Depth-D leaves keep the exact
+// per-child self test (bh_child).
+#ifndef BH_SC_THETA
+#define BH_SC_THETA 0.7  // (A/B builds: -1 turns the correction off)
+#endif
+constexpr double kScTheta = BH_SC_THETA;
+
+template <int D>
+__device__ __forceinline__ bool self_leaf_above_D(const void *codes, int64_t t,
+                                                  int64_t n) {
+    using K = typename std::conditional<D == 16, uint32_t, uint64_t>::type;
+    const K *sc = (const K *)codes;
+    auto same = [&](int64_t u) -> int {
+        if (u <= 0 || u >= n) return -1;
+        const K x = sc[u] ^ sc[u - 1];
+        if (x == 0) return D;
+        const int lz = sizeof(K) == 4 ? __clz((unsigned)x)
+                                      : __clzll((unsigned long long)x);
+        return lz >> 1;
+    };
+    // leaf depth of point t: min(D, 1 + max(same[t], same[t+1])) (tree.cu)
+    return 1 + max(same(t), same(t + 1)) < D;
+}
 
 #ifndef BH_REP_MIN_BLOCKS
 // 9 CTAs x 4 warps per SM (56 registers).  With 8-warp CTAs: 5 per SM
@@ -218,7 +254,7 @@ struct RepArgs {
 #endif
 
 // CTA `bid` of the `nblk` traversal CTAs: points t_begin + 256 bid + [0, 256).
-template <int D, bool COUNT, bool QUERY>
+template <int D, bool COUNT, bool QUERY, bool SC>
 __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
                                           int64_t nblk) {
     constexpr int CAP = 3 * D + 2;
@@ -272,17 +308,17 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         // the branch-free body above the deepest level (warp-uniform)
         if (BH_REP_FAST && ent.w < (uint32_t)D) {
             switch (cnt) {
-                case 1: bh_group<1, COUNT, true>(g, first, a, cn, stk, sp); break;
-                case 2: bh_group<2, COUNT, true>(g, first, a, cn, stk, sp); break;
-                case 3: bh_group<3, COUNT, true>(g, first, a, cn, stk, sp); break;
-                default: bh_group<4, COUNT, true>(g, first, a, cn, stk, sp); break;
+                case 1: bh_group<1, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
+                case 2: bh_group<2, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
+                case 3: bh_group<3, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
+                default: bh_group<4, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
             }
         } else {
             switch (cnt) {
-                case 1: bh_group<1, COUNT, false>(g, first, a, cn, stk, sp); break;
-                case 2: bh_group<2, COUNT, false>(g, first, a, cn, stk, sp); break;
-                case 3: bh_group<3, COUNT, false>(g, first, a, cn, stk, sp); break;
-                default: bh_group<4, COUNT, false>(g, first, a, cn, stk, sp); break;
+                case 1: bh_group<1, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
+                case 2: bh_group<2, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
+                case 3: bh_group<3, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
+                default: bh_group<4, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
             }
         }
         z = a.z;
@@ -291,6 +327,8 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         __syncwarp();
     }
 
+    if (SC && valid && self_leaf_above_D<D>(A.codes, t, A.n_points))
+        z -= 1.0;
     if (valid) {
         const int64_t o = A.sorted_out ? t - t_begin : (int64_t)order[t];
         A.rep[o] = make_float2((float)r0, (float)r1);
@@ -301,13 +339,13 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
                A.z_out);
 }
 
-template <int D, bool COUNT, bool QUERY>
+template <int D, bool COUNT, bool QUERY, bool SC>
 __global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
 k_repulsive(const RepArgs A) {
     bh_pdl_trigger();  // the successor may launch early (PDL)
     bh_pdl_wait();     // the predecessor's results are visible
 
-    rep_block<D, COUNT, QUERY>(A, blockIdx.x, gridDim.x);
+    rep_block<D, COUNT, QUERY, SC>(A, blockIdx.x, gridDim.x);
 }
 // Sum of gathered per-CTA Z partials into *out (one warp, fixed order).
 __global__ void k_fixed_sum(const double *__restrict__ x, int64_t n,
@@ -431,7 +469,7 @@ k_attractive(const AttArgs A) {
 // Each CTA computes exactly what it computes in its own kernel; the Z
 // partials are indexed by traversal CTA, so Z is bitwise the same.
 // ---------------------------------------------------------------------------
-template <int D, int G, bool PADDED>
+template <int D, int G, bool PADDED, bool SC>
 __global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
 k_forces(const RepArgs R, const AttArgs A, int64_t nr, int64_t na) {
     bh_pdl_trigger();  // the successor may launch early (PDL)
@@ -442,7 +480,7 @@ k_forces(const RepArgs R, const AttArgs A, int64_t nr, int64_t na) {
     if (upto > before)
         att_block<G, PADDED, kRepThreads>(A, before, na);
     else
-        rep_block<D, false, false>(R, b - upto, nr);
+        rep_block<D, false, false, SC>(R, b - upto, nr);
 }
 
 // ---------------------------------------------------------------------------
@@ -584,14 +622,20 @@ extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
     const RepArgs A{(const float4 *)t->node, (const float2 *)t->ys, t->order,
                     (const float2 *)y_query, bounds, t->status, theta, t_begin,
                     t_end, sorted_out, (float2 *)rep, zpart, (int4 *)counts,
-                    zblock, ticket, z_out};
-#define BH_REP_LAUNCH(D, CNT, Q)                                              \
-    BH_LAUNCH("k_repulsive", (k_repulsive<D, CNT, Q>), grid, kRepThreads, 0, st, A)
+                    zblock, ticket, z_out, t->sorted_codes, t->n_points};
+    const bool sc = theta <= kScTheta;
+#define BH_REP_LAUNCH(D, CNT, Q, SC)                                          \
+    BH_LAUNCH("k_repulsive", (k_repulsive<D, CNT, Q, SC>), grid, kRepThreads, 0, st, A)
 #define BH_REP_LAUNCH2(D)                                                     \
     if (y_query) {                                                            \
-        if (counts) BH_REP_LAUNCH(D, true, true); else BH_REP_LAUNCH(D, false, true); \
+        if (counts) BH_REP_LAUNCH(D, true, true, false);                      \
+        else BH_REP_LAUNCH(D, false, true, false);                            \
+    } else if (sc) {                                                          \
+        if (counts) BH_REP_LAUNCH(D, true, false, true);                      \
+        else BH_REP_LAUNCH(D, false, false, true);                            \
     } else {                                                                  \
-        if (counts) BH_REP_LAUNCH(D, true, false); else BH_REP_LAUNCH(D, false, false); \
+        if (counts) BH_REP_LAUNCH(D, true, false, false);                     \
+        else BH_REP_LAUNCH(D, false, false, false);                           \
     }
     if (t->code_bits == 32) {
         BH_REP_LAUNCH2(16)
@@ -699,18 +743,24 @@ extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
     const RepArgs R{(const float4 *)t->node, (const float2 *)t->ys, t->order,
                     nullptr, bounds, t->status, theta, t_begin, t_end,
                     sorted_out, (float2 *)rep, nullptr, nullptr, zblock, ticket,
-                    z_out};
+                    z_out, t->sorted_codes, t->n_points};
     const AttArgs A{row_ptr, col, val, (const float2 *)y, row_begin, row_end,
                     exaggeration, sched, (float2 *)attr};
     cudaStream_t st = bh_cs(stream);
     const unsigned grid = (unsigned)(nr + na);
-#define BH_FORCES(D)                                                          \
+#define BH_FORCES1(D, SC)                                                     \
     if (padded)                                                               \
-        BH_LAUNCH("k_forces", (k_forces<D, G, true>), grid, kRepThreads, 0,   \
-                  st, R, A, nr, na);                                          \
+        BH_LAUNCH("k_forces", (k_forces<D, G, true, SC>), grid, kRepThreads,  \
+                  0, st, R, A, nr, na);                                       \
     else                                                                      \
-        BH_LAUNCH("k_forces", (k_forces<D, G, false>), grid, kRepThreads, 0,  \
-                  st, R, A, nr, na);
+        BH_LAUNCH("k_forces", (k_forces<D, G, false, SC>), grid, kRepThreads, \
+                  0, st, R, A, nr, na);
+#define BH_FORCES(D)                                                          \
+    if (theta <= kScTheta) {                                                  \
+        BH_FORCES1(D, true)                                                   \
+    } else {                                                                  \
+        BH_FORCES1(D, false)                                                  \
+    }
     if (t->code_bits == 32) {
         BH_FORCES(16)
     } else if (t->code_bits == 64) {
@@ -719,6 +769,7 @@ extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
         return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
     }
 #undef BH_FORCES
+#undef BH_FORCES1
     BH_CHECK_LAUNCH("k_forces");
     return BH_OK;
 }
