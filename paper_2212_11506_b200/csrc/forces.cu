@@ -104,6 +104,22 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
     return need;
 }
 
+// p ? x : 0 as one select on the f32 value (kept ahead of the f64
+// conversion, which the compiler otherwise selects twice per double)
+__device__ __forceinline__ float sel_f32(bool p, float x) {
+    float r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+        "selp.f32 %0, %1, 0f00000000, q;\n\t}"
+        : "=f"(r) : "f"(x), "r"((uint32_t)p));
+    return r;
+}
+
+#ifndef BH_REP_PUSH_BALLOT
+// 1: the pushing lanes find their stack slots with one ballot; 0: the
+// push mask is assembled from the per-child ballots
+#define BH_REP_PUSH_BALLOT 1
+#endif
+
 #ifndef BH_REP_FAST
 // 1: groups above the deepest level (no coincident-code buckets there) use
 // bh_child_fast, one branch-free body per child; 0: bh_child everywhere
@@ -169,6 +185,31 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
         pm[c] = FAST ? bh_child_fast<COUNT, SC>(g, rec[c], fz, fx, fy, cn)
                      : bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
     }
+#if BH_REP_PUSH_BALLOT
+    if (FAST) {  // out-of-mask lanes add nothing (exact zero, in f32)
+        fz = sel_f32(g.mine, fz);
+        fx = sel_f32(g.mine, fx);
+        fy = sel_f32(g.mine, fy);
+    }
+    a64.z += (double)fz;
+    a64.r0 += (double)fx;
+    a64.r1 += (double)fy;
+    // lane c < CNT pushes child c's group if any lane must open it; one
+    // ballot gives every writer its slot (child 0 ends on top)
+    uint32_t info = inf[0], msk = pm[0];
+#pragma unroll
+    for (int c = 1; c < CNT; c++)
+        if (g.lane == c) {
+            info = inf[c];
+            msk = pm[c];
+        }
+    const bool push = g.lane < CNT && msk != 0u;
+    const uint32_t nz = ballot_full(push);
+    if (push)
+        stk[sp + __popc(nz >> (g.lane + 1))] = make_uint4(
+            info, msk, __float_as_uint(g.r2 * 0.25f), g.depth + 1u);
+    sp += __popc(nz);
+#else
     if (FAST && !g.mine) fz = fx = fy = 0.f;  // exact: nothing of this group
     a64.z += (double)fz;
     a64.r0 += (double)fx;
@@ -191,6 +232,7 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
         }
         sp += __popc(nz);
     }
+#endif
 }
 
 // Stack entry (16 B, one STS.128 / broadcast LDS.128): x = the opened
