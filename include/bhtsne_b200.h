@@ -92,7 +92,7 @@ typedef struct bh_sched_t {
 
 /* Node record of the level-contiguous quadtree (16 bytes):
  *   x, y  : centre of mass (float32, quadtree.py:488-508)
- *   mass  : point count (uint32 bits)
+ *   mass  : point count (float32 value; exact below 2^24 points)
  *   info  : bit 31 = leaf; leaf -> bits 0..30 = first point (sorted order);
  *           internal -> bits 0..28 = first child node, bits 29..30 =
  *           (number of children - 1).  Children of a node are consecutive

@@ -98,11 +98,14 @@ template <> __device__ __forceinline__ double2 mk2<double>(double a, double b) {
 // {com.x, com.y, mass, info}; f64 trees two, {com.x, com.y} (f64) then
 // {mass, info, 0, 0}.
 template <typename T> struct NodeRec;
+// f32 records hold the point count as a float (exact below 2^24 points;
+// the f32 traversal weighs a cell by float(mass) in any case), so the
+// traversal reads its weight without a conversion per child
 template <> struct NodeRec<float> {
     static constexpr int kWords = 1;
     __device__ static void store(void *base, int64_t i, float2 c, uint32_t m,
                                  uint32_t info) {
-        ((float4 *)base)[i] = make_float4(c.x, c.y, __uint_as_float(m),
+        ((float4 *)base)[i] = make_float4(c.x, c.y, __uint2float_rn(m),
                                           __uint_as_float(info));
     }
     __device__ static void store_info(void *base, int64_t i, uint32_t info) {
@@ -112,7 +115,7 @@ template <> struct NodeRec<float> {
         return __float_as_uint(((const float4 *)base)[i].w);
     }
     __device__ static uint32_t mass(const void *base, int64_t i) {
-        return __float_as_uint(((const float4 *)base)[i].z);
+        return __float2uint_rn(((const float4 *)base)[i].z);
     }
     __device__ static float2 com(const void *base, int64_t i) {
         const float4 r = ((const float4 *)base)[i];

@@ -46,7 +46,7 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
                                              float &fz, float &fx, float &fy,
                                              Acc64 &a64, RepCounts &cn) {
     const uint32_t info = __float_as_uint(r.w);
-    const uint32_t m = __float_as_uint(r.z);
+    const uint32_t m = __float2uint_rn(r.z);  // point count (f32 record)
     const float dx = g.yi.x - r.x, dy = g.yi.y - r.y;
     const float d2 = fmaf(dx, dx, dy * dy);
     float w;
@@ -93,7 +93,7 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
             cn.internal++;
             cn.accepted += acc;
         }
-        w = (g.mine && acc) ? __uint2float_rn(m) : 0.f;
+        w = (g.mine && acc) ? r.z : 0.f;
         need = ballot_full(g.mine && !acc);
     }
     const float k = rcp_approx(1.0f + d2);
@@ -139,7 +139,6 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
                                                   float &fx, float &fy,
                                                   RepCounts &cn) {
     const uint32_t info = __float_as_uint(r.w);
-    const uint32_t m = __float_as_uint(r.z);
     const float dx = g.yi.x - r.x, dy = g.yi.y - r.y;
     const float d2 = fmaf(dx, dx, dy * dy);
     const bool leaf = (int32_t)info < 0;
@@ -147,7 +146,7 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
     if (COUNT && g.mine) {
         if (leaf) {
             cn.leafnodes++;
-            cn.leafpts += (int)m;
+            cn.leafpts += (int)r.z;
         } else {
             cn.internal++;
             cn.accepted += acc;
@@ -157,7 +156,7 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
     // the self leaf is not tested here: it adds exactly k = 1/(1+0) = 1 to
     // z and 0 to the force, and rep_block subtracts that 1 (SelfCorr)
     const bool use = acc && (SC || info != (BH_LEAF_BIT | g.self));
-    const float w = use ? __uint2float_rn(m) : 0.f;
+    const float w = use ? r.z : 0.f;  // the cell's point count
     const uint32_t need = ballot_full(g.mine && !acc);
     const float k = rcp_approx(1.0f + d2);
     const float wk = w * k, wk2 = wk * k;
@@ -349,12 +348,15 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         // straight-line code for the (warp-uniform) number of children;
         // the branch-free body above the deepest level (warp-uniform)
         if (BH_REP_FAST && ent.w < (uint32_t)D) {
-            switch (cnt) {
-                case 1: bh_group<1, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
-                case 2: bh_group<2, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
-                case 3: bh_group<3, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
-                default: bh_group<4, COUNT, true, SC>(g, first, a, cn, stk, sp); break;
-            }
+            // most groups are full (4 children): test that first
+            if (__builtin_expect(cnt == 4, 1))
+                bh_group<4, COUNT, true, SC>(g, first, a, cn, stk, sp);
+            else if (cnt == 3)
+                bh_group<3, COUNT, true, SC>(g, first, a, cn, stk, sp);
+            else if (cnt == 2)
+                bh_group<2, COUNT, true, SC>(g, first, a, cn, stk, sp);
+            else
+                bh_group<1, COUNT, true, SC>(g, first, a, cn, stk, sp);
         } else {
             switch (cnt) {
                 case 1: bh_group<1, COUNT, false, SC>(g, first, a, cn, stk, sp); break;

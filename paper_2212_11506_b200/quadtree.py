@@ -238,7 +238,7 @@ class MortonQuadtree:
             mass, info = (mi[:, 0].astype(np.int64), mi[:, 1].astype(np.int64))
         else:
             info = rec[:, 3].view(np.uint32).astype(np.int64)
-            mass = rec[:, 2].view(np.uint32).astype(np.int64)
+            mass = rec[:, 2].astype(np.int64)  # f32 records: float count
         is_leaf = ((info & _lib.BH_LEAF_BIT) != 0).astype(np.uint8)
         start = self.arrays.node_start[:m].cpu().numpy().astype(np.int64)
         parent = self.arrays.parent[:m].cpu().numpy().astype(np.int64)
