@@ -337,8 +337,11 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         __syncwarp();
     }
     while (sp > 0) {
+        // (no barrier after the read: every lane's ballots below depend on
+        // `ent`, so all reads complete before any lane overwrites the slot;
+        // the barrier at the end of the loop orders the pushes before the
+        // next read)
         const uint4 ent = stk[--sp];
-        __syncwarp();
         const uint32_t first = ent.x & BH_CHILD_MASK;
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const bool mine = (ent.y >> lane) & 1u;

@@ -233,6 +233,24 @@ def full_run_c0():
     print("c0 kl", kl, timings.kl_history)
 
 
+def full_run_c0_seeds():
+    """C0 full f32 runs of the reference for Y0 seeds 0..7: the spread of
+    the final KL over equally valid (chaotic) trajectories, beside which
+    the 1% KL criterion is checked on a median (test_gpu_parity.py)."""
+    import bhtsne
+    sys.path.insert(0, REPO)
+    from paper_2212_11506_b200.workloads import c0
+    x = c0()
+    kls = []
+    for seed in range(8):
+        cfg = bhtsne.TsneConfig(precision="f32", seed=seed, threads=8)
+        _, _, kl = bhtsne.run(bhtsne.InputMatrix(x), cfg)
+        kls.append(kl)
+    np.savez_compressed(os.path.join(HERE, "c0_seeds.npz"),
+                        seeds=np.arange(8), kl=np.array(kls))
+    print("c0 seeds kl", kls)
+
+
 def full_run_c1():
     """C1 (BASELINE.json configs[1], N=70k, D=50) full 1000-iteration f32
     run of the reference: its KL and periodic KL (the final-KL parity at a
@@ -278,6 +296,8 @@ def main():
             affinity_f64()
         elif what == "c0":
             full_run_c0()
+        elif what == "c0_seeds":
+            full_run_c0_seeds()
         elif what == "c1":
             full_run_c1()
         elif what == "c2":

@@ -378,6 +378,26 @@ def test_c0_full_run_kl_within_1pct(bh):
                             knn=(idx, sqd))
     assert abs(kl - float(g["kl"])) / float(g["kl"]) < 0.01, kl
     assert timings.calls("tree") == 1000
+
+
+@pytest.mark.slow
+def test_c0_seed_median_kl_within_1pct(bh):
+    """The trajectory is chaotic: any change of f32 summation order gives
+    another, equally valid one (the reference's own final KL over Y0 seeds
+    0..7 spans 1.6565..1.6815).  The 1% criterion on a statistic that does
+    not hinge on one trajectory: the median final KL over the same 8 seeds,
+    ours against the unmodified reference's (tests/golden c0_seeds)."""
+    from paper_2212_11506_b200.workloads import c0
+    from oracle import oracle as o
+    ref = golden("c0_seeds")["kl"].astype(np.float64)
+    x = c0()
+    idx, sqd = o.knn_exact(x, 90)
+    ours = [bh.run(x, bh.TsneConfig(seed=s), knn=(idx, sqd))[2]
+            for s in range(len(ref))]
+    med_o, med_r = float(np.median(ours)), float(np.median(ref))
+    assert abs(med_o - med_r) / med_r < 0.01, (ours, ref.tolist())
+    # every one of our runs inside the reference's seed range, widened by 1%
+    assert min(ours) > 0.99 * ref.min() and max(ours) < 1.01 * ref.max(), ours
     assert [it for it, _ in timings.kl_history] == [250, 500, 750, 1000]
     # and through the GPU kNN (run without a graph)
     e2, _, kl2 = bh.run(c0(), bh.TsneConfig())
