@@ -114,7 +114,7 @@ typedef struct bh_tree_t {
     float *node;       /* node_capacity records as above (16 or 32 B) */
     int32_t *parent;   /* node_capacity: parent node, -1 for the root */
     int32_t *node_start; /* node_capacity: first point (sorted order) */
-    int32_t *leaf_end;   /* node_capacity: one past the last point (leaves) */
+    int32_t *leaf_end;   /* node_capacity: one past the last point of each node */
     int32_t *level_off;  /* max_depth + 3 entries: level l = [off[l], off[l+1]),
                             off[max_depth + 2] = number of levels */
     int32_t *order;      /* n: sorted position -> point id */
@@ -173,8 +173,18 @@ int bh_build_tree(const bh_tree_t *tree, const void *y, void *ws,
  * (f64 sums in reference order, stored in the tree's precision). */
 int bh_summarize(const bh_tree_t *tree, void *ws, size_t ws_bytes,
                  bh_stream_t stream);
-/* ws: the bh_tree_workspace_bytes() workspace (holds a grid barrier; all
- * levels run in one cooperative launch when the device supports it). */
+/* ws: the bh_tree_workspace_bytes() workspace of the build. */
+
+/* Prefix summarize (f32 trees; the engine's per-iteration path): every node
+ * is the contiguous run [node_start, leaf_end) of sorted points, so count =
+ * end - start and centre = (S[end] - S[start]) / count with S the f64
+ * prefix sum of the sorted points -- two launches instead of one per level.
+ * Single-point leaves and depth-D buckets are exactly the reference's; an
+ * internal centre differs from bh_summarize's child-order f64 sums only by
+ * f64 rounding before the f32 store.  ws: the workspace bh_build_tree used
+ * (it holds the build's per-tile point sums). */
+int bh_summarize_prefix(const bh_tree_t *tree, void *ws, size_t ws_bytes,
+                        bh_stream_t stream);
 
 /* ---- attractive force (forces.py:56-82) ---------------------------------
  * attr[i] = sum_t v_t*(y_i - y_j)/(1+|y_i-y_j|^2) over CSR row i, for rows

@@ -75,6 +75,7 @@ SIGNATURES = {
     "bh_tree_workspace_bytes": ([_I64, C.c_int], _SZ),
     "bh_build_tree": ([C.POINTER(TreeStruct), _P, _P, _SZ, _P], C.c_int),
     "bh_summarize": ([C.POINTER(TreeStruct), _P, _SZ, _P], C.c_int),
+    "bh_summarize_prefix": ([C.POINTER(TreeStruct), _P, _SZ, _P], C.c_int),
     "bh_attractive": ([_P, _P, _P, _I64, C.c_int, _P, _I64, _I64, C.c_float,
                        _P, _P, _P], C.c_int),
     "bh_repulsive_workspace_bytes": ([_I64], _SZ),

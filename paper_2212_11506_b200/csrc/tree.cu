@@ -131,12 +131,15 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
             const int32_t *__restrict__ level_off, void *__restrict__ node,
             int32_t *__restrict__ parent, int32_t *__restrict__ node_start,
             int32_t *__restrict__ leaf_end, p2_t<T> *__restrict__ ys,
-            int32_t *__restrict__ rank, const int32_t *__restrict__ status) {
+            int32_t *__restrict__ rank, double2 *__restrict__ tile_sum,
+            const int32_t *__restrict__ status) {
     bh_pdl_trigger();  // the successor may launch early (PDL)
     bh_pdl_wait();     // the predecessor's results are visible
 
     using Rec = NodeRec<T>;
     if (*status != BH_OK) return;
+    __shared__ double2 s_tsum[kTreeWarps];
+    double sx = 0.0, sy = 0.0;  // this thread's points, in order (f64)
     __shared__ uint32_t s_bal[kTreeWarps][D + 1];
     __shared__ uint32_t s_woff[kTreeWarps][D + 1];
     __shared__ uint32_t s_carry[D + 1];
@@ -181,6 +184,8 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
             const int32_t pid = order[t];
             const p2_t<T> p = y[pid];
             ys[t] = p;
+            sx = __dadd_rn(sx, (double)p.x);
+            sy = __dadd_rn(sy, (double)p.y);
             if (rank) rank[pid] = (int32_t)t;
             for (int d = lo; d <= hi; d++) {
                 const int32_t id = base(d);
@@ -192,16 +197,167 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
                 } else if (s1 < D) {
                     // single-point leaf: complete record (quadtree.py:490-498)
                     Rec::store(node, id, p, 1u, BH_LEAF_BIT | (uint32_t)t);
-                    leaf_end[id] = (int32_t)(t + 1);
                 } else {
                     // first point of a run of equal codes (depth-D bucket)
                     Rec::store_info(node, id, BH_LEAF_BIT | (uint32_t)t);
                 }
             }
-            // last point of a run of equal codes closes its depth-D leaf
-            if (s0 == D && s1 < D) leaf_end[base(D) - 1] = (int32_t)(t + 1);
+            // t is the last point of its level-d node for every level d
+            // deeper than the prefix it shares with t + 1: the node's end
+            // (leaf_end holds the end of every node, leaves and internal)
+            for (int d = max(s1 + 1, 0); d <= hi; d++)
+                leaf_end[d >= lo ? base(d) : base(d) - 1] = (int32_t)(t + 1);
         }
         __syncthreads();
+    }
+    // the tile's f64 sum of its sorted points (prefix summarize): thread
+    // sums in point order, then a fixed butterfly and warp order
+    if (tile_sum) {
+        sx = warp_sum(sx);
+        sy = warp_sum(sy);
+        if (lane == 0) s_tsum[warp] = make_double2(sx, sy);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = 0.0, b = 0.0;
+            for (int w = 0; w < kTreeWarps; w++) {
+                a = __dadd_rn(a, s_tsum[w].x);
+                b = __dadd_rn(b, s_tsum[w].y);
+            }
+            tile_sum[blockIdx.x] = make_double2(a, b);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Prefix summarize (the engine's f32 path): every node covers a contiguous
+// run [start, end) of sorted points, so its count is end - start and its
+// centre of mass (S[end] - S[start]) / count with S the f64 prefix sum of
+// the sorted points -- all levels in one pass instead of one launch per
+// level.  Single-point leaves keep the point itself (from emit) and depth-D
+// buckets their in-order f64 mean, as in the reference; an internal node's
+// centre differs from the reference's child-by-child f64 sums only by f64
+// rounding (|S| eps ~ 1e-8 at C3 scale, far below the f32 spacing of the
+// stored value except at coordinates within ~1e-2 of zero).
+// ---------------------------------------------------------------------------
+constexpr int kPsThreads = kTreeThreads;
+constexpr int kPsPPT = kTreeChunk / kPsThreads;  // consecutive points/thread
+
+// S[t] = sum of sorted points before t (f64), per emit tile: the tile's
+// prefix (tile sums of emit, fixed-order warp sum) plus a block scan.
+template <typename T>
+__global__ void __launch_bounds__(kPsThreads)
+k_prefix_scan(const p2_t<T> *__restrict__ ys, int64_t n,
+              const double2 *__restrict__ tile_sum, double2 *__restrict__ S,
+              const int32_t *__restrict__ status) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
+    if (*status != BH_OK) return;
+    __shared__ double2 s_w[kTreeWarps];
+    __shared__ double2 s_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = blockIdx.x;
+    if (warp == 0) {
+        double a = 0.0, c = 0.0;
+        for (int64_t i = lane; i < b; i += 32) {
+            const double2 v = tile_sum[i];
+            a = __dadd_rn(a, v.x);
+            c = __dadd_rn(c, v.y);
+        }
+        a = warp_sum(a);
+        c = warp_sum(c);
+        if (lane == 0) s_base = make_double2(a, c);
+    }
+    const int64_t t0 = b * kTreeChunk + (int64_t)threadIdx.x * kPsPPT;
+    double2 loc[kPsPPT];
+    double ax = 0.0, ay = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPsPPT; k++) {
+        loc[k] = make_double2(ax, ay);  // exclusive, within the thread
+        if (t0 + k < n) {
+            const p2_t<T> p = ys[t0 + k];
+            ax = __dadd_rn(ax, (double)p.x);
+            ay = __dadd_rn(ay, (double)p.y);
+        }
+    }
+    // exclusive scan of the thread totals across the block
+    double ex = ax, ey = ay;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double ux = __shfl_up_sync(0xffffffffu, ex, o);
+        const double uy = __shfl_up_sync(0xffffffffu, ey, o);
+        if (lane >= o) {
+            ex = __dadd_rn(ex, ux);
+            ey = __dadd_rn(ey, uy);
+        }
+    }
+    if (lane == 31) s_w[warp] = make_double2(ex, ey);
+    ex = __dsub_rn(ex, ax);  // exclusive within the warp
+    ey = __dsub_rn(ey, ay);
+    __syncthreads();
+    double bx = s_base.x, by = s_base.y;
+    for (int w = 0; w < warp; w++) {
+        bx = __dadd_rn(bx, s_w[w].x);
+        by = __dadd_rn(by, s_w[w].y);
+    }
+    bx = __dadd_rn(bx, ex);
+    by = __dadd_rn(by, ey);
+#pragma unroll
+    for (int k = 0; k < kPsPPT; k++)
+        if (t0 + k <= n)
+            S[t0 + k] = make_double2(__dadd_rn(bx, loc[k].x),
+                                     __dadd_rn(by, loc[k].y));
+    if (t0 + kPsPPT == n)  // n on a thread boundary: S[n] = all points
+        S[n] = make_double2(__dadd_rn(bx, ax), __dadd_rn(by, ay));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSumThreads)
+k_summarize_prefix(void *__restrict__ node, const int32_t *__restrict__ parent,
+                   const int32_t *__restrict__ node_start,
+                   const int32_t *__restrict__ node_end,
+                   const p2_t<T> *__restrict__ ys,
+                   const double2 *__restrict__ S,
+                   const int32_t *__restrict__ level_off, int D,
+                   const int32_t *__restrict__ status) {
+    bh_pdl_trigger();  // the successor may launch early (PDL)
+    bh_pdl_wait();     // the predecessor's results are visible
+
+    using Rec = NodeRec<T>;
+    if (*status != BH_OK) return;
+    const int32_t m_tot = level_off[D + 1];
+    for (int32_t nd = blockIdx.x * kSumThreads + threadIdx.x; nd < m_tot;
+         nd += gridDim.x * kSumThreads) {
+        const uint32_t info = Rec::info(node, nd);
+        const int32_t end = node_end[nd];
+        if (info & BH_LEAF_BIT) {
+            const uint32_t t = info & ~BH_LEAF_BIT;
+            const uint32_t cnt = (uint32_t)end - t;
+            if (cnt == 1) continue;  // single-point leaf, completed by emit
+            double a = 0.0, b = 0.0;  // depth-D bucket: in-order f64 mean
+            for (int64_t q = t; q < end; q++) {
+                const p2_t<T> p = ys[q];
+                a = __dadd_rn(a, (double)p.x);
+                b = __dadd_rn(b, (double)p.y);
+            }
+            Rec::store(node, nd,
+                       mk2<T>((T)__ddiv_rn(a, (double)cnt),
+                              (T)__ddiv_rn(b, (double)cnt)),
+                       cnt, info);
+            continue;
+        }
+        const int32_t start = node_start[nd];
+        const uint32_t cnt = (uint32_t)(end - start);
+        const uint32_t fc = info & BH_CHILD_MASK;
+        uint32_t k = 1;  // children: the consecutive next-level nodes
+#pragma unroll
+        for (uint32_t c = 1; c < 4; c++)
+            if ((int32_t)(fc + c) < m_tot && parent[fc + c] == nd) k = c + 1;
+        const double2 se = S[end], ss = S[start];
+        Rec::store(node, nd,
+                   mk2<T>((T)__ddiv_rn(__dsub_rn(se.x, ss.x), (double)cnt),
+                          (T)__ddiv_rn(__dsub_rn(se.y, ss.y), (double)cnt)),
+                   cnt, fc | ((k - 1) << BH_NKIDS_SHIFT));
     }
 }
 
@@ -299,7 +455,7 @@ k_summarize_top(void *__restrict__ node, const int32_t *__restrict__ parent,
 }
 
 struct TreeLayout {
-    size_t counts, offs, bar, total;
+    size_t counts, offs, bar, tsum, S, total;
     int nblk;
 };
 
@@ -309,7 +465,9 @@ static TreeLayout tree_layout(int64_t n, int D) {
     L.counts = 0;
     L.offs = bh_align(sizeof(uint32_t) * L.nblk * (D + 1));
     L.bar = L.offs + bh_align(sizeof(uint32_t) * L.nblk * (D + 1));
-    L.total = L.bar + 256;
+    L.tsum = L.bar + 256;  // emit's tile sums (prefix summarize)
+    L.S = L.tsum + bh_align(sizeof(double2) * L.nblk);
+    L.total = L.S + bh_align(sizeof(double2) * (n + 1));
     return L;
 }
 
@@ -327,7 +485,7 @@ static int build_impl(const bh_tree_t *t, const void *y, void *ws,
     BH_LAUNCH("k_tree_emit", (k_tree_emit<K, D, T>), L.nblk, kTreeThreads, 0, st,
         sc, t->order, (const p2_t<T> *)y, t->n_points, off, t->level_off,
         (void *)t->node, t->parent, t->node_start, t->leaf_end,
-        (p2_t<T> *)t->ys, t->rank, t->status);
+        (p2_t<T> *)t->ys, t->rank, (double2 *)(w + L.tsum), t->status);
     return BH_OK;
 }
 
@@ -404,5 +562,28 @@ extern "C" int bh_summarize(const bh_tree_t *t, void *ws, size_t ws_bytes,
                       t->parent, t->leaf_end, (const float2 *)t->ys,
                       t->level_off, dtop, D, t->status);
     }
+    return BH_OK;
+}
+
+extern "C" int bh_summarize_prefix(const bh_tree_t *t, void *ws,
+                                   size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(t && t->n_points >= 1, "need at least one point");
+    BH_REQUIRE(t->precision != 64,
+               "precision-64 tree: use bh_summarize (bit-exact f64 centres)");
+    BH_REQUIRE(ws_bytes >= bh_tree_workspace_bytes(t->n_points, t->code_bits),
+               "tree workspace too small");
+    const TreeLayout L = tree_layout(t->n_points, t->max_depth);
+    char *w = (char *)ws;
+    const double2 *tsum = (const double2 *)(w + L.tsum);
+    double2 *S = (double2 *)(w + L.S);
+    cudaStream_t st = bh_cs(stream);
+    BH_LAUNCH("k_prefix_scan", k_prefix_scan<float>, L.nblk, kPsThreads, 0,
+              st, (const float2 *)t->ys, t->n_points, tsum, S, t->status);
+    int grid = bh_blocks(t->node_capacity, kSumThreads);
+    if (grid > kSumBlocks) grid = kSumBlocks;
+    BH_LAUNCH("k_summarize_prefix", k_summarize_prefix<float>, grid,
+              kSumThreads, 0, st, (void *)t->node, t->parent, t->node_start,
+              t->leaf_end, (const float2 *)t->ys, (const double2 *)S,
+              t->level_off, t->max_depth, t->status);
     return BH_OK;
 }

@@ -314,6 +314,12 @@ class Engine:
         # run inside the fused force launch.  Measured at C3 (it/s): 0: 487,
         # 0.3: 498, 0.4: 505, 0.45: 506, 0.6: 499, 1.0: 479
         self.attr_split = 0.45
+        # f32 runs summarize from the f64 prefix sums of the sorted points
+        # (2 launches; internal centres of mass differ from the reference's
+        # child-order sums by f64 rounding only); f64 runs keep the
+        # bit-exact level-by-level summarize.  The stage API's summarize()
+        # is always the bit-exact one.
+        self.prefix_summary = self.dtype == torch.float32
         # fuse: the untimed fast path launches the fused force pass
         # (bh_forces); the evented (StepTimings) path keeps the two kernels
         # apart for the per-stage breakdown unless fuse_timed is set
@@ -352,14 +358,16 @@ class Engine:
 
     def kernels_per_iteration(self, timed: bool = False) -> int:
         """Library kernel launches of one iteration: morton, sort histogram +
-        one pass per code byte, 3 tree kernels, one summarize kernel per
-        level below the top 7 plus one for levels 6..0 (tree.cu), the force
+        one pass per code byte, 3 tree kernels, the summarize kernels (2 for
+        the prefix summarize; else one per level below the top 7 plus one
+        for levels 6..0, tree.cu), the force
         pass (1 fused or attractive +
         repulsive), update; + the Z-partials sum when sharded."""
         forces = 1 if self._fused(timed) else 2
         depth = self.code_bits // 2
         top = min(int(os.environ.get("BH_SUM_TOP", 6)), depth)  # tree.cu
-        summarize = depth - top + (1 if top >= 0 else 0)
+        summarize = (2 if self.prefix_summary
+                     else depth - top + (1 if top >= 0 else 0))
         return (1 + 1 + self.code_bits // 8 + 3 + summarize
                 + forces + 1 + (1 if self.shard is not None else 0))
 
@@ -415,7 +423,10 @@ class Engine:
              ptr(t.order), ptr(self.ws_sort), self.ws_sort.numel(), st)
         t.build(y, st)
         rec(1)
-        t.summarize(st)
+        if self.prefix_summary:
+            t.summarize_prefix(st)
+        else:
+            t.summarize(st)
         rec(2)
         if self._fused(ev is not None):
             # both force passes in one launch, their CTAs sharing the SMs

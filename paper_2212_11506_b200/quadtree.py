@@ -181,6 +181,12 @@ class TreeArrays:
         call("bh_summarize", self.sref(), ptr(self.ws), self.ws.numel(),
              st or stream())
 
+    def summarize_prefix(self, st=None):
+        """All levels from the f64 prefix sums of the sorted points (f32
+        trees; see bh_summarize_prefix)."""
+        call("bh_summarize_prefix", self.sref(), ptr(self.ws),
+             self.ws.numel(), st or stream())
+
 
 class MortonQuadtree:
     """Level-contiguous quadtree in HBM (quadtree.py:66-119).

@@ -89,6 +89,50 @@ def test_tree_bit_exact_vs_oracle_large(bh, oracle, mode, kind):
         np.testing.assert_array_equal(out[f], getattr(ot, f), err_msg=f)
 
 
+@pytest.mark.parametrize("mode", [32, 64])
+@pytest.mark.parametrize("kind", ["gauss", "heavy", "dups", "tiny_spread"])
+@pytest.mark.parametrize("n", [120_000, 4096, 2049])
+def test_prefix_summarize_matches_exact(bh, mode, kind, n):
+    """The engine's f32 summarize from f64 prefix sums against the bit-exact
+    level-by-level one: counts, child words and leaf centres bitwise;
+    internal centres within 2 f32 spacings (f64 rounding only)."""
+    rng = np.random.default_rng(hash((mode, kind, n)) % 2**32)
+    if kind == "gauss":
+        y = rng.standard_normal((n, 2))
+    elif kind == "heavy":
+        c = rng.uniform(-50, 50, (100, 2))
+        y = c[rng.integers(0, 100, n)] + rng.standard_t(2.0, (n, 2))
+    elif kind == "dups":
+        base = rng.standard_normal((max(1, n // 50), 2))
+        y = base[rng.integers(0, len(base), n)]
+    else:
+        y = 1e3 + rng.standard_normal((n, 2)) * 1e-5
+    y = y.astype(np.float32)
+    _, _, t = gpu_tree(bh, y, mode)
+    a = t.arrays
+    m = int(a.level_off[a.max_depth + 1].item())
+    exact = a.node[:m].cpu().numpy().copy()
+    a.summarize_prefix()
+    torch.cuda.synchronize()
+    pref = a.node[:m].cpu().numpy()
+    np.testing.assert_array_equal(pref[:, 2:].view(np.uint32),
+                                  exact[:, 2:].view(np.uint32))
+    leaf = (exact[:, 3].view(np.uint32) & np.uint32(0x80000000)) != 0
+    np.testing.assert_array_equal(pref[leaf, :2].view(np.uint32),
+                                  exact[leaf, :2].view(np.uint32))
+    # internal centres: within one f32 spacing of the true f64 mean of the
+    # node's points (the reference's child-order sums of f32-rounded child
+    # centres drift by up to ~one spacing per level, hence no bitwise check)
+    ys = a.ys.cpu().numpy().astype(np.float64)
+    S = np.concatenate([np.zeros((1, 2)), np.cumsum(ys, axis=0)])
+    start = a.node_start[:m].cpu().numpy().astype(np.int64)[~leaf]
+    end = a.leaf_end[:m].cpu().numpy().astype(np.int64)[~leaf]
+    true = (S[end] - S[start]) / (end - start)[:, None]
+    np.testing.assert_array_equal(end - start, pref[~leaf, 2].astype(np.int64))
+    d = np.abs(pref[~leaf, :2].astype(np.float64) - true)
+    assert (d <= np.spacing(np.abs(true).astype(np.float32))).all(), d.max()
+
+
 @pytest.mark.parametrize("bits", [8, 17, 32, 42, 64])
 def test_radix_sort_is_stable_argsort(bh, bits):
     from paper_2212_11506_b200 import _lib
@@ -376,8 +420,17 @@ def test_c0_full_run_kl_within_1pct(bh):
     idx, sqd = o.knn_exact(c0(), 90)
     e, timings, kl = bh.run(c0(), bh.TsneConfig(kl_every=250),
                             knn=(idx, sqd))
-    assert abs(kl - float(g["kl"])) / float(g["kl"]) < 0.01, kl
+    # one chaotic trajectory: its final KL must fall inside the spread of the
+    # reference's own runs over Y0 seeds 0..7 (widened by 1%); the 1%
+    # criterion itself is checked on the 8-seed median below
+    ref = golden("c0_seeds")["kl"].astype(np.float64)
+    assert float(g["kl"]) == ref[0]
+    assert 0.99 * ref.min() < kl < 1.01 * ref.max(), kl
     assert timings.calls("tree") == 1000
+    assert [it for it, _ in timings.kl_history] == [250, 500, 750, 1000]
+    # and through the GPU kNN (run without a graph)
+    e2, _, kl2 = bh.run(c0(), bh.TsneConfig())
+    np.testing.assert_array_equal(e2.y.cpu().numpy(), e.y.cpu().numpy())
 
 
 @pytest.mark.slow
@@ -398,10 +451,6 @@ def test_c0_seed_median_kl_within_1pct(bh):
     assert abs(med_o - med_r) / med_r < 0.01, (ours, ref.tolist())
     # every one of our runs inside the reference's seed range, widened by 1%
     assert min(ours) > 0.99 * ref.min() and max(ours) < 1.01 * ref.max(), ours
-    assert [it for it, _ in timings.kl_history] == [250, 500, 750, 1000]
-    # and through the GPU kNN (run without a graph)
-    e2, _, kl2 = bh.run(c0(), bh.TsneConfig())
-    np.testing.assert_array_equal(e2.y.cpu().numpy(), e.y.cpu().numpy())
 
 
 @pytest.mark.slow
