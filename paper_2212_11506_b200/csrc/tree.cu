@@ -29,7 +29,10 @@ namespace bh {
 
 constexpr int kTreeThreads = 256;
 constexpr int kTreeWarps = kTreeThreads / 32;
-constexpr int kTreePPT = 8;  // sub-chunks per CTA
+#ifndef BH_TREE_PPT
+#define BH_TREE_PPT 8
+#endif
+constexpr int kTreePPT = BH_TREE_PPT;  // sub-chunks per CTA
 constexpr int kTreeChunk = kTreeThreads * kTreePPT;
 constexpr int kSumThreads = 256;
 constexpr int kSumBlocks = kSMs * 8;

@@ -103,7 +103,14 @@ def child(args):
            "repulsive_ms": timeit(rep, args.reps),
            "forces_fused_ms": timeit(fused, args.reps),
            "sort_build_ms": timeit(sort_build, args.reps),
+           "sort_ms": timeit(lambda: call(
+               "bh_sort", ptr(eng.codes), eng.n, 32, ptr(t.sorted_codes),
+               ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st),
+               args.reps),
            "summarize_ms": timeit(lambda: t.summarize(), args.reps)}
+    if args.precision == "f32":
+        out["summarize_prefix_ms"] = timeit(lambda: t.summarize_prefix(),
+                                            args.reps)
     print(json.dumps(out), flush=True)
 
 
