@@ -38,10 +38,55 @@ struct GroupCtx {
     uint32_t depth;  // of the group's children
 };
 
+// p ? x : 0 as one select on the f32 value (kept ahead of the f64
+// conversion, which the compiler otherwise selects twice per double)
+__device__ __forceinline__ float sel_f32(bool p, float x) {
+    float r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+        "selp.f32 %0, %1, 0f00000000, q;\n\t}"
+        : "=f"(r) : "f"(x), "r"((uint32_t)p));
+    return r;
+}
+
+#ifndef BH_REP_PUSH_BALLOT
+// 1: the pushing lanes find their stack slots with one ballot; 0: the
+// push mask is assembled from the per-child ballots
+#define BH_REP_PUSH_BALLOT 1
+#endif
+
+// The m > 1 points [s, s + m) of a depth-D bucket leaf (coincident codes)
+// for one lane (forces.py:102-110): loaded once per 32 and broadcast by
+// shuffles; f32 partials per 32 points, then f64.  Self is skipped by index
+// unless SC (its exact +1 to z is then subtracted at the end).
+template <bool SC>
+__device__ __forceinline__ void bh_bucket(const GroupCtx &g, uint32_t s,
+                                          uint32_t m, Acc64 &a64) {
+    for (uint32_t b = 0; b < m; b += 32) {
+        const float2 pq = (b + g.lane < m) ? g.ys[s + b + g.lane]
+                                           : make_float2(0.f, 0.f);
+        const int nb = (int)min(32u, m - b);
+        float bz = 0.f, bx = 0.f, by = 0.f;
+        for (int jj = 0; jj < nb; jj++) {
+            const float px = __shfl_sync(0xffffffffu, pq.x, jj);
+            const float py = __shfl_sync(0xffffffffu, pq.y, jj);
+            const float ex = g.yi.x - px, ey = g.yi.y - py;
+            const float kk = rcp_approx(1.0f + fmaf(ex, ex, ey * ey));
+            const float ww = (SC || s + b + jj != g.self) ? kk : 0.f;
+            const float ww2 = ww * kk;
+            bz += ww;
+            bx = fmaf(ww2, ex, bx);
+            by = fmaf(ww2, ey, by);
+        }
+        a64.z += (double)sel_f32(g.mine, bz);
+        a64.r0 += (double)sel_f32(g.mine, bx);
+        a64.r1 += (double)sel_f32(g.mine, by);
+    }
+}
+
 // One child for one lane (the reference rule, forces.py:99-128).  Returns
 // the ballot of lanes that must open it (0 for leaves); the lane's f32
 // contribution goes to (fz, fx, fy), a bucket leaf's straight into a64.
-template <bool COUNT>
+template <bool COUNT, bool SC>
 __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
                                              float &fz, float &fx, float &fy,
                                              Acc64 &a64, RepCounts &cn) {
@@ -57,34 +102,13 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
             cn.leafnodes++;
             cn.leafpts += (int)m;
         }
-        if (m > 1u) {
-            // coincident-code bucket at max depth (warp-uniform, rare):
-            // points loaded once per 32 and broadcast by shuffles
-            for (uint32_t b = 0; b < m; b += 32) {
-                const float2 pq = (b + g.lane < m) ? g.ys[s + b + g.lane]
-                                                   : make_float2(0.f, 0.f);
-                const int nb = (int)min(32u, m - b);
-                float bz = 0.f, bx = 0.f, by = 0.f;
-                for (int jj = 0; jj < nb; jj++) {
-                    const float px = __shfl_sync(0xffffffffu, pq.x, jj);
-                    const float py = __shfl_sync(0xffffffffu, pq.y, jj);
-                    const float ex = g.yi.x - px, ey = g.yi.y - py;
-                    const float kk = rcp_approx(1.0f + fmaf(ex, ex, ey * ey));
-                    const float ww = (g.mine && s + b + jj != g.self) ? kk : 0.f;
-                    const float ww2 = ww * kk;
-                    bz += ww;
-                    bx = fmaf(ww2, ex, bx);
-                    by = fmaf(ww2, ey, by);
-                }
-                a64.z += (double)bz;
-                a64.r0 += (double)bx;
-                a64.r1 += (double)by;
-            }
+        if (m > 1u) {  // coincident-code bucket at max depth (warp-uniform)
+            bh_bucket<SC>(g, s, m, a64);
             return 0;
         }
         // single-point leaf: direct interaction unless it is self
         // (info == LEAF_BIT | first point; compare the whole word)
-        w = (g.mine && info != (BH_LEAF_BIT | g.self)) ? 1.f : 0.f;
+        w = (g.mine && (SC || info != (BH_LEAF_BIT | g.self))) ? 1.f : 0.f;
     } else {
         // accepted iff d2 > R2 (R2 = side^2 / theta^2): the reference's
         // (2r)^2 < theta^2 d^2 (forces.py:112-116)
@@ -103,22 +127,6 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
     fy = fmaf(wk2, dy, fy);
     return need;
 }
-
-// p ? x : 0 as one select on the f32 value (kept ahead of the f64
-// conversion, which the compiler otherwise selects twice per double)
-__device__ __forceinline__ float sel_f32(bool p, float x) {
-    float r;
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-        "selp.f32 %0, %1, 0f00000000, q;\n\t}"
-        : "=f"(r) : "f"(x), "r"((uint32_t)p));
-    return r;
-}
-
-#ifndef BH_REP_PUSH_BALLOT
-// 1: the pushing lanes find their stack slots with one ballot; 0: the
-// push mask is assembled from the per-child ballots
-#define BH_REP_PUSH_BALLOT 1
-#endif
 
 #ifndef BH_REP_FAST
 // 1: groups above the deepest level (no coincident-code buckets there) use
@@ -154,7 +162,7 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
     }
     // lanes outside the mask are zeroed once per group (bh_group); with SC
     // the self leaf is not tested here: it adds exactly k = 1/(1+0) = 1 to
-    // z and 0 to the force, and rep_block subtracts that 1 (SelfCorr)
+    // z and 0 to the force, and rep_block subtracts that 1 (kScTheta)
     const bool use = acc && (SC || info != (BH_LEAF_BIT | g.self));
     const float w = use ? r.z : 0.f;  // the cell's point count
     const uint32_t need = ballot_full(g.mine && !acc);
@@ -182,7 +190,7 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
     for (int c = 0; c < CNT; c++) {
         inf[c] = __float_as_uint(rec[c].w);
         pm[c] = FAST ? bh_child_fast<COUNT, SC>(g, rec[c], fz, fx, fy, cn)
-                     : bh_child<COUNT>(g, rec[c], fz, fx, fy, a64, cn);
+                     : bh_child<COUNT, SC>(g, rec[c], fz, fx, fy, a64, cn);
     }
 #if BH_REP_PUSH_BALLOT
     if (FAST) {  // out-of-mask lanes add nothing (exact zero, in f32)
@@ -254,38 +262,20 @@ struct RepArgs {
     double *__restrict__ zblock;
     unsigned *__restrict__ ticket;
     double *__restrict__ z_out;
-    const void *__restrict__ codes;  // sorted codes (self correction)
-    int64_t n_points;
 };
 
 // Self correction (SC): when theta <= kScTheta no point accepts an
 // ancestor of its own leaf -- d^2 <= (2 sqrt2 r)^2 = 8 r^2 for the point and
 // the centre of mass inside one cell, while acceptance needs d^2 >
-// 4 r^2 / theta^2 >= 8.16 r^2 -- so every point whose leaf lies above depth
-// D (a single-point leaf, visited by the branch-free body) meets it exactly
-// once and its +1 is subtracted at the end.  Depth-D leaves keep the exact
-// per-child self test (bh_child).
+// 4 r^2 / theta^2 >= 8.16 r^2 -- so every point meets itself exactly once,
+// in its own leaf (single-point or depth-D bucket), where the pair term is
+// k = 1/(1+0) = 1 to z and 0 to the force.  No child or bucket point is
+// then tested against self; rep_block subtracts the 1 at the end.  Above
+// kScTheta the exact per-child / per-point self test stays.
 #ifndef BH_SC_THETA
 #define BH_SC_THETA 0.7  // (A/B builds: -1 turns the correction off)
 #endif
 constexpr double kScTheta = BH_SC_THETA;
-
-template <int D>
-__device__ __forceinline__ bool self_leaf_above_D(const void *codes, int64_t t,
-                                                  int64_t n) {
-    using K = typename std::conditional<D == 16, uint32_t, uint64_t>::type;
-    const K *sc = (const K *)codes;
-    auto same = [&](int64_t u) -> int {
-        if (u <= 0 || u >= n) return -1;
-        const K x = sc[u] ^ sc[u - 1];
-        if (x == 0) return D;
-        const int lz = sizeof(K) == 4 ? __clz((unsigned)x)
-                                      : __clzll((unsigned long long)x);
-        return lz >> 1;
-    };
-    // leaf depth of point t: min(D, 1 + max(same[t], same[t+1])) (tree.cu)
-    return 1 + max(same(t), same(t + 1)) < D;
-}
 
 #ifndef BH_REP_MIN_BLOCKS
 // 9 CTAs x 4 warps per SM (56 registers).  With 8-warp CTAs: 5 per SM
@@ -374,8 +364,7 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         __syncwarp();
     }
 
-    if (SC && valid && self_leaf_above_D<D>(A.codes, t, A.n_points))
-        z -= 1.0;
+    if (SC && valid) z -= 1.0;  // the self leaf's exact +1 (kScTheta)
     if (valid) {
         const int64_t o = A.sorted_out ? t - t_begin : (int64_t)order[t];
         A.rep[o] = make_float2((float)r0, (float)r1);
@@ -669,7 +658,7 @@ extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
     const RepArgs A{(const float4 *)t->node, (const float2 *)t->ys, t->order,
                     (const float2 *)y_query, bounds, t->status, theta, t_begin,
                     t_end, sorted_out, (float2 *)rep, zpart, (int4 *)counts,
-                    zblock, ticket, z_out, t->sorted_codes, t->n_points};
+                    zblock, ticket, z_out};
     const bool sc = theta <= kScTheta;
 #define BH_REP_LAUNCH(D, CNT, Q, SC)                                          \
     BH_LAUNCH("k_repulsive", (k_repulsive<D, CNT, Q, SC>), grid, kRepThreads, 0, st, A)
@@ -790,7 +779,7 @@ extern "C" int bh_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
     const RepArgs R{(const float4 *)t->node, (const float2 *)t->ys, t->order,
                     nullptr, bounds, t->status, theta, t_begin, t_end,
                     sorted_out, (float2 *)rep, nullptr, nullptr, zblock, ticket,
-                    z_out, t->sorted_codes, t->n_points};
+                    z_out};
     const AttArgs A{row_ptr, col, val, (const float2 *)y, row_begin, row_end,
                     exaggeration, sched, (float2 *)attr};
     cudaStream_t st = bh_cs(stream);
