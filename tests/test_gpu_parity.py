@@ -6,6 +6,8 @@ and centres of mass bit-exact; per-iteration gradients <= 1e-4 relative L2;
 BSP betas <= 1e-5 relative; final KL within 1%.
 """
 
+import zlib
+
 import numpy as np
 import pytest
 
@@ -65,7 +67,7 @@ def test_golden_dump(bh):
 @pytest.mark.parametrize("mode", [32, 64])
 @pytest.mark.parametrize("kind", ["gauss", "heavy", "dups", "tiny_spread"])
 def test_tree_bit_exact_vs_oracle_large(bh, oracle, mode, kind):
-    rng = np.random.default_rng(hash((mode, kind)) % 2**32)
+    rng = np.random.default_rng(zlib.crc32(f"{mode}-{kind}".encode()))
     n = 120_000
     if kind == "gauss":
         y = rng.standard_normal((n, 2))
@@ -96,7 +98,7 @@ def test_prefix_summarize_matches_exact(bh, mode, kind, n):
     """The engine's f32 summarize from f64 prefix sums against the bit-exact
     level-by-level one: counts, child words and leaf centres bitwise;
     internal centres within 2 f32 spacings (f64 rounding only)."""
-    rng = np.random.default_rng(hash((mode, kind, n)) % 2**32)
+    rng = np.random.default_rng(zlib.crc32(f"{mode}-{kind}-{n}".encode()))
     if kind == "gauss":
         y = rng.standard_normal((n, 2))
     elif kind == "heavy":
@@ -129,8 +131,12 @@ def test_prefix_summarize_matches_exact(bh, mode, kind, n):
     end = a.leaf_end[:m].cpu().numpy().astype(np.int64)[~leaf]
     true = (S[end] - S[start]) / (end - start)[:, None]
     np.testing.assert_array_equal(end - start, pref[~leaf, 2].astype(np.int64))
-    d = np.abs(pref[~leaf, :2].astype(np.float64) - true)
-    assert (d <= np.spacing(np.abs(true).astype(np.float32))).all(), d.max()
+    got = pref[~leaf, :2].astype(np.float64)
+    d = np.abs(got - true)
+    # one spacing of the f32 grid at the larger magnitude (a truth just
+    # below a power of two may round up into the next binade)
+    ulp = np.spacing(np.maximum(np.abs(true), np.abs(got)).astype(np.float32))
+    assert (d <= ulp).all(), d.max()
 
 
 @pytest.mark.parametrize("bits", [8, 17, 32, 42, 64])
