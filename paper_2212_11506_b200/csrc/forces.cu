@@ -341,8 +341,10 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         // straight-line code for the (warp-uniform) number of children;
         // the branch-free body above the deepest level (warp-uniform)
         if (BH_REP_FAST && ent.w < (uint32_t)D) {
-            // most groups are full (4 children): test that first
-            if (__builtin_expect(cnt == 4, 1))
+            // most groups are full (4 children): test that first, on the
+            // raw word (info bits 29-30 = 3; a compare the compiler does
+            // not fold into a jump table with the other counts)
+            if (__builtin_expect(ent.x >= (3u << BH_NKIDS_SHIFT), 1))
                 bh_group<4, COUNT, true, SC>(g, first, a, cn, stk, sp);
             else if (cnt == 3)
                 bh_group<3, COUNT, true, SC>(g, first, a, cn, stk, sp);
