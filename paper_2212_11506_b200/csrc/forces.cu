@@ -141,7 +141,7 @@ __device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
 // it "accepts" unconditionally (minus self, compared by the whole info
 // word); an internal node accepts iff d2 > R2.  Same decisions and
 // contributions as bh_child.
-template <bool COUNT, bool SC>
+template <bool COUNT, bool SC, bool FIRST = false>
 __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
                                                   const float4 r, float &fz,
                                                   float &fx, float &fy,
@@ -168,9 +168,15 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
     const uint32_t need = ballot_full(g.mine && !acc);
     const float k = rcp_approx(1.0f + d2);
     const float wk = w * k, wk2 = wk * k;
-    fz += wk;
-    fx = fmaf(wk2, dx, fx);
-    fy = fmaf(wk2, dy, fy);
+    if (FIRST) {  // the group's first term starts the partials (no 0 + x)
+        fz = wk;
+        fx = wk2 * dx;
+        fy = wk2 * dy;
+    } else {
+        fz += wk;
+        fx = fmaf(wk2, dx, fx);
+        fy = fmaf(wk2, dy, fy);
+    }
     return need;
 }
 
@@ -189,8 +195,9 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
 #pragma unroll
     for (int c = 0; c < CNT; c++) {
         inf[c] = __float_as_uint(rec[c].w);
-        pm[c] = FAST ? bh_child_fast<COUNT, SC>(g, rec[c], fz, fx, fy, cn)
-                     : bh_child<COUNT, SC>(g, rec[c], fz, fx, fy, a64, cn);
+        pm[c] = !FAST ? bh_child<COUNT, SC>(g, rec[c], fz, fx, fy, a64, cn)
+                : c == 0 ? bh_child_fast<COUNT, SC, true>(g, rec[c], fz, fx, fy, cn)
+                         : bh_child_fast<COUNT, SC>(g, rec[c], fz, fx, fy, cn);
     }
 #if BH_REP_PUSH_BALLOT
     if (FAST) {  // out-of-mask lanes add nothing (exact zero, in f32)
@@ -313,6 +320,7 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
     double r0 = 0.0, r1 = 0.0, z = 0.0;
     RepCounts cn = {0, 0, 0, 0};
     uint4 *stk = s_stack[warp];
+    Acc64 a{0.0, 0.0, 0.0};
 
     int sp = 0;
     if (act) {
@@ -337,7 +345,6 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         const bool mine = (ent.y >> lane) & 1u;
         const float r2 = __uint_as_float(ent.z);
         const GroupCtx g{node, ys, yi, r2, mine, self, lane, ent.w};
-        Acc64 a{z, r0, r1};
         // straight-line code for the (warp-uniform) number of children;
         // the branch-free body above the deepest level (warp-uniform)
         if (BH_REP_FAST && ent.w < (uint32_t)D) {
@@ -360,11 +367,11 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
                 default: bh_group<4, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
             }
         }
-        z = a.z;
-        r0 = a.r0;
-        r1 = a.r1;
         __syncwarp();
     }
+    z = a.z;
+    r0 = a.r0;
+    r1 = a.r1;
 
     if (SC && valid) z -= 1.0;  // the self leaf's exact +1 (kScTheta)
     if (valid) {
