@@ -514,8 +514,14 @@ k_attractive(const AttArgs A) {
 // Each CTA computes exactly what it computes in its own kernel; the Z
 // partials are indexed by traversal CTA, so Z is bitwise the same.
 // ---------------------------------------------------------------------------
+#ifndef BH_FORCES_MIN_BLOCKS
+// 10 CTAs/SM for the fused pass (48 registers): its sweep CTAs gain more
+// co-residency than the traversal CTAs lose (C3 iteration 600: 1.338 vs
+// 1.450 ms at 9; the traversal alone prefers 9, BH_REP_MIN_BLOCKS)
+#define BH_FORCES_MIN_BLOCKS 10
+#endif
 template <int D, int G, bool PADDED, bool SC>
-__global__ void __launch_bounds__(kRepThreads, BH_REP_MIN_BLOCKS)
+__global__ void __launch_bounds__(kRepThreads, BH_FORCES_MIN_BLOCKS)
 k_forces(const RepArgs R, const AttArgs A, int64_t nr, int64_t na) {
     bh_pdl_trigger();  // the successor may launch early (PDL)
     bh_pdl_wait();     // the predecessor's results are visible

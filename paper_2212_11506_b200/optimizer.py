@@ -312,8 +312,10 @@ class Engine:
         # fraction of the CSR rows swept on the (low-priority) side stream
         # under the latency-bound tree build in the fused fast path; the rest
         # run inside the fused force launch.  Measured at C3 (it/s): 0: 487,
-        # 0.3: 498, 0.4: 505, 0.45: 506, 0.6: 499, 1.0: 479
-        self.attr_split = 0.45
+        # 0.3: 498, 0.4: 505, 0.45: 506, 0.6: 499, 1.0: 479 (round-1 v10);
+        # after the traversal rework and the 10-CTA fused pass: 0.2: 612,
+        # 0.25: 614, 0.3: 619, 0.35: 620, 0.4: 618, 0.45: 613, 0.55: 602
+        self.attr_split = 0.35
         # f32 runs summarize from the f64 prefix sums of the sorted points
         # (2 launches; internal centres of mass differ from the reference's
         # child-order sums by f64 rounding only); f64 runs keep the
