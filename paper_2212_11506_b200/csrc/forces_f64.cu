@@ -139,31 +139,33 @@ __device__ __forceinline__ void rep_block64(const RepArgs64 &A, int64_t bid,
         __syncwarp();
     }
     while (sp > 0) {
+        // (no barrier after the read: the ballots below depend on `ent` in
+        // every lane; the barrier at the end orders the pushes)
         const uint4 ent = stk[--sp];
-        __syncwarp();
         const uint32_t first = ent.x & BH_CHILD_MASK;
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const double side2 = __longlong_as_double(
             (long long)(((unsigned long long)ent.w << 32) | ent.z));
         const Ctx64 g{A.node, A.ys, yi, side2, theta2, ((ent.y >> lane) & 1u) != 0,
                       (uint32_t)t, lane};
-        uint32_t info = 0, msk = 0, nz = 0;
+        uint32_t info = 0, msk = 0;
         for (int c = 0; c < cnt; c++) {  // warp-uniform trip count
             const double2 cc = __ldg((const double2 *)A.node + 2 * (first + c));
             const uint4 mi = __ldg((const uint4 *)A.node + 2 * (first + c) + 1);
             const uint32_t need = bh_child64<COUNT>(g, cc, mi.x, mi.y, a, cn);
-            nz |= (need != 0u ? 1u : 0u) << c;
             if (lane == c) {
                 info = mi.y;
                 msk = need;
             }
         }
-        if (nz) {
-            if (msk)
-                stk[sp + __popc(nz >> (lane + 1))] =
-                    side2_entry(info, msk, __dmul_rn(side2, 0.25));
-            sp += __popc(nz);
-        }
+        // lane c pushes child c's group if any lane opens it; one ballot
+        // gives every writer its slot (child 0 ends on top)
+        const bool push = msk != 0u;
+        const uint32_t nz = ballot_full(push);
+        if (push)
+            stk[sp + __popc(nz >> (lane + 1))] =
+                side2_entry(info, msk, __dmul_rn(side2, 0.25));
+        sp += __popc(nz);
         __syncwarp();
     }
     if (valid) {
