@@ -84,6 +84,30 @@ __device__ __forceinline__ uint32_t bh_child64(const Ctx64 &g, double2 c,
     return ballot_full(g.mine && !acc);
 }
 
+// The CNT children of one popped group, in order (the reference's
+// accumulation order); lane c keeps child c's info word and push mask.
+template <int CNT, bool COUNT>
+__device__ __forceinline__ void group64(const Ctx64 &g, const void *node,
+                                        uint32_t first, Acc64 &a,
+                                        RepCounts &cn, uint32_t &info,
+                                        uint32_t &msk) {
+    double2 cc[CNT];
+    uint2 mi[CNT];
+#pragma unroll
+    for (int c = 0; c < CNT; c++) {
+        cc[c] = __ldg((const double2 *)node + 2 * (first + c));
+        mi[c] = __ldg((const uint2 *)node + 4 * (first + c) + 2);
+    }
+#pragma unroll
+    for (int c = 0; c < CNT; c++) {
+        const uint32_t need = bh_child64<COUNT>(g, cc[c], mi[c].x, mi[c].y, a, cn);
+        if (g.lane == c) {
+            info = mi[c].y;
+            msk = need;
+        }
+    }
+}
+
 struct RepArgs64 {
     const void *__restrict__ node;
     const double2 *__restrict__ ys;
@@ -149,15 +173,16 @@ __device__ __forceinline__ void rep_block64(const RepArgs64 &A, int64_t bid,
         const Ctx64 g{A.node, A.ys, yi, side2, theta2, ((ent.y >> lane) & 1u) != 0,
                       (uint32_t)t, lane};
         uint32_t info = 0, msk = 0;
-        for (int c = 0; c < cnt; c++) {  // warp-uniform trip count
-            const double2 cc = __ldg((const double2 *)A.node + 2 * (first + c));
-            const uint4 mi = __ldg((const uint4 *)A.node + 2 * (first + c) + 1);
-            const uint32_t need = bh_child64<COUNT>(g, cc, mi.x, mi.y, a, cn);
-            if (lane == c) {
-                info = mi.y;
-                msk = need;
-            }
-        }
+        // straight-line code per (warp-uniform) child count, every record of
+        // the group loaded up front; full groups tested first on the raw word
+        if (ent.x >= (3u << BH_NKIDS_SHIFT))
+            group64<4, COUNT>(g, A.node, first, a, cn, info, msk);
+        else if (cnt == 3)
+            group64<3, COUNT>(g, A.node, first, a, cn, info, msk);
+        else if (cnt == 2)
+            group64<2, COUNT>(g, A.node, first, a, cn, info, msk);
+        else
+            group64<1, COUNT>(g, A.node, first, a, cn, info, msk);
         // lane c pushes child c's group if any lane opens it; one ballot
         // gives every writer its slot (child 0 ends on top)
         const bool push = msk != 0u;
