@@ -48,12 +48,6 @@ __device__ __forceinline__ float sel_f32(bool p, float x) {
     return r;
 }
 
-#ifndef BH_REP_PUSH_BALLOT
-// 1: the pushing lanes find their stack slots with one ballot; 0: the
-// push mask is assembled from the per-child ballots
-#define BH_REP_PUSH_BALLOT 1
-#endif
-
 // The m > 1 points [s, s + m) of a depth-D bucket leaf (coincident codes)
 // for one lane (forces.py:102-110): loaded once per 32 and broadcast by
 // shuffles; f32 partials per 32 points, then f64.  Self is skipped by index
@@ -83,64 +77,14 @@ __device__ __forceinline__ void bh_bucket(const GroupCtx &g, uint32_t s,
     }
 }
 
-// One child for one lane (the reference rule, forces.py:99-128).  Returns
-// the ballot of lanes that must open it (0 for leaves); the lane's f32
-// contribution goes to (fz, fx, fy), a bucket leaf's straight into a64.
-template <bool COUNT, bool SC>
-__device__ __forceinline__ uint32_t bh_child(const GroupCtx &g, const float4 r,
-                                             float &fz, float &fx, float &fy,
-                                             Acc64 &a64, RepCounts &cn) {
-    const uint32_t info = __float_as_uint(r.w);
-    const uint32_t m = __float2uint_rn(r.z);  // point count (f32 record)
-    const float dx = g.yi.x - r.x, dy = g.yi.y - r.y;
-    const float d2 = fmaf(dx, dx, dy * dy);
-    float w;
-    uint32_t need = 0;
-    if (info & BH_LEAF_BIT) {  // warp-uniform
-        const uint32_t s = info & ~BH_LEAF_BIT;
-        if (COUNT && g.mine) {
-            cn.leafnodes++;
-            cn.leafpts += (int)m;
-        }
-        if (m > 1u) {  // coincident-code bucket at max depth (warp-uniform)
-            bh_bucket<SC>(g, s, m, a64);
-            return 0;
-        }
-        // single-point leaf: direct interaction unless it is self
-        // (info == LEAF_BIT | first point; compare the whole word)
-        w = (g.mine && (SC || info != (BH_LEAF_BIT | g.self))) ? 1.f : 0.f;
-    } else {
-        // accepted iff d2 > R2 (R2 = side^2 / theta^2): the reference's
-        // (2r)^2 < theta^2 d^2 (forces.py:112-116)
-        const bool acc = d2 > g.r2;
-        if (COUNT && g.mine) {
-            cn.internal++;
-            cn.accepted += acc;
-        }
-        w = (g.mine && acc) ? r.z : 0.f;
-        need = ballot_full(g.mine && !acc);
-    }
-    const float k = rcp_approx(1.0f + d2);
-    const float wk = w * k, wk2 = wk * k;
-    fz += wk;
-    fx = fmaf(wk2, dx, fx);
-    fy = fmaf(wk2, dy, fy);
-    return need;
-}
-
-#ifndef BH_REP_FAST
-// 1: groups above the deepest level (no coincident-code buckets there) use
-// bh_child_fast, one branch-free body per child; 0: bh_child everywhere
-#define BH_REP_FAST 1
-#endif
-
-// bh_child for a group whose children are above depth D, where every leaf
+// One child of a group above depth D for one lane (the reference rule,
+// forces.py:99-128), where every leaf
 // holds exactly one point (leaf iff count == 1 or depth == D,
 // quadtree.py:262-300).  Leaf vs internal is folded into the predicates: a
 // leaf is never approximated and its record is its point with mass 1, so
 // it "accepts" unconditionally (minus self, compared by the whole info
 // word); an internal node accepts iff d2 > R2.  Same decisions and
-// contributions as bh_child.
+// contributions as the reference's per-point walk.
 template <bool COUNT, bool SC, bool FIRST = false>
 __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
                                                   const float4 r, float &fz,
@@ -180,10 +124,11 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
     return need;
 }
 
-// Visit the CNT consecutive children starting at `first`, then push every
-// child some lane must open in one lane-parallel step (lane c writes child
-// c's entry; child 0 ends on top so the first subtree is popped first).
-template <int CNT, bool COUNT, bool FAST, bool SC>
+// Visit the CNT consecutive children starting at `first` (a group above
+// depth D), then push every child some lane must open in one lane-parallel
+// step (lane c writes child c's entry; child 0 ends on top so the first
+// subtree is popped first).
+template <int CNT, bool COUNT, bool SC>
 __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
                                          Acc64 &a64, RepCounts &cn,
                                          uint4 *stk, int &sp) {
@@ -195,19 +140,13 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
 #pragma unroll
     for (int c = 0; c < CNT; c++) {
         inf[c] = __float_as_uint(rec[c].w);
-        pm[c] = !FAST ? bh_child<COUNT, SC>(g, rec[c], fz, fx, fy, a64, cn)
-                : c == 0 ? bh_child_fast<COUNT, SC, true>(g, rec[c], fz, fx, fy, cn)
-                         : bh_child_fast<COUNT, SC>(g, rec[c], fz, fx, fy, cn);
+        pm[c] = c == 0 ? bh_child_fast<COUNT, SC, true>(g, rec[c], fz, fx, fy, cn)
+                       : bh_child_fast<COUNT, SC>(g, rec[c], fz, fx, fy, cn);
     }
-#if BH_REP_PUSH_BALLOT
-    if (FAST) {  // out-of-mask lanes add nothing (exact zero, in f32)
-        fz = sel_f32(g.mine, fz);
-        fx = sel_f32(g.mine, fx);
-        fy = sel_f32(g.mine, fy);
-    }
-    a64.z += (double)fz;
-    a64.r0 += (double)fx;
-    a64.r1 += (double)fy;
+    // out-of-mask lanes add nothing (exact zero, in f32)
+    a64.z += (double)sel_f32(g.mine, fz);
+    a64.r0 += (double)sel_f32(g.mine, fx);
+    a64.r1 += (double)sel_f32(g.mine, fy);
     // lane c < CNT pushes child c's group if any lane must open it; one
     // ballot gives every writer its slot (child 0 ends on top)
     uint32_t info = inf[0], msk = pm[0];
@@ -223,30 +162,43 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
         stk[sp + __popc(nz >> (g.lane + 1))] = make_uint4(
             info, msk, __float_as_uint(g.r2 * 0.25f), g.depth + 1u);
     sp += __popc(nz);
-#else
-    if (FAST && !g.mine) fz = fx = fy = 0.f;  // exact: nothing of this group
-    a64.z += (double)fz;
-    a64.r0 += (double)fx;
-    a64.r1 += (double)fy;
-    uint32_t nz = 0;
+}
+
+// A group at depth D (max depth): every child is a leaf -- a single point
+// or a coincident-code bucket (quadtree.py leaf rule) -- so there is no
+// acceptance test, no ballot and nothing to push.
+template <int CNT, bool COUNT, bool SC>
+__device__ __forceinline__ void bh_group_leaves(const GroupCtx &g,
+                                                uint32_t first, Acc64 &a64,
+                                                RepCounts &cn) {
+    float4 rec[CNT];
 #pragma unroll
-    for (int c = 0; c < CNT; c++) nz |= (pm[c] != 0u ? 1u : 0u) << c;
-    if (nz) {
-        if (g.lane < CNT && ((nz >> g.lane) & 1u)) {
-            uint32_t info = inf[0], msk = pm[0];
+    for (int c = 0; c < CNT; c++) rec[c] = __ldg(&g.node[first + c]);
+    float fz = 0.f, fx = 0.f, fy = 0.f;
 #pragma unroll
-            for (int c = 1; c < CNT; c++)
-                if (g.lane == c) {
-                    info = inf[c];
-                    msk = pm[c];
-                }
-            stk[sp + __popc(nz >> (g.lane + 1))] =
-                make_uint4(info, msk, __float_as_uint(g.r2 * 0.25f),
-                           g.depth + 1u);
+    for (int c = 0; c < CNT; c++) {
+        const uint32_t info = __float_as_uint(rec[c].w);
+        const uint32_t m = __float2uint_rn(rec[c].z);
+        if (COUNT && g.mine) {
+            cn.leafnodes++;
+            cn.leafpts += (int)m;
         }
-        sp += __popc(nz);
+        if (m > 1u) {  // bucket (warp-uniform)
+            bh_bucket<SC>(g, info & ~BH_LEAF_BIT, m, a64);
+        } else {
+            const float dx = g.yi.x - rec[c].x, dy = g.yi.y - rec[c].y;
+            const float k = rcp_approx(1.0f + fmaf(dx, dx, dy * dy));
+            // self: exact test, or SC's +1 subtracted at the end
+            const float w = (SC || info != (BH_LEAF_BIT | g.self)) ? k : 0.f;
+            const float w2 = w * k;
+            fz += w;
+            fx = fmaf(w2, dx, fx);
+            fy = fmaf(w2, dy, fy);
+        }
     }
-#endif
+    a64.z += (double)sel_f32(g.mine, fz);
+    a64.r0 += (double)sel_f32(g.mine, fx);
+    a64.r1 += (double)sel_f32(g.mine, fy);
 }
 
 // Stack entry (16 B, one STS.128 / broadcast LDS.128): x = the opened
@@ -347,25 +299,28 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         const GroupCtx g{node, ys, yi, r2, mine, self, lane, ent.w};
         // straight-line code for the (warp-uniform) number of children;
         // the branch-free body above the deepest level (warp-uniform)
-        if (BH_REP_FAST && ent.w < (uint32_t)D) {
+        if (ent.w < (uint32_t)D) {
             // most groups are full (4 children): test that first, on the
             // raw word (info bits 29-30 = 3; a compare the compiler does
             // not fold into a jump table with the other counts)
             if (__builtin_expect(ent.x >= (3u << BH_NKIDS_SHIFT), 1))
-                bh_group<4, COUNT, true, SC>(g, first, a, cn, stk, sp);
+                bh_group<4, COUNT, SC>(g, first, a, cn, stk, sp);
             else if (cnt == 3)
-                bh_group<3, COUNT, true, SC>(g, first, a, cn, stk, sp);
+                bh_group<3, COUNT, SC>(g, first, a, cn, stk, sp);
             else if (cnt == 2)
-                bh_group<2, COUNT, true, SC>(g, first, a, cn, stk, sp);
+                bh_group<2, COUNT, SC>(g, first, a, cn, stk, sp);
             else
-                bh_group<1, COUNT, true, SC>(g, first, a, cn, stk, sp);
+                bh_group<1, COUNT, SC>(g, first, a, cn, stk, sp);
         } else {
-            switch (cnt) {
-                case 1: bh_group<1, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
-                case 2: bh_group<2, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
-                case 3: bh_group<3, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
-                default: bh_group<4, COUNT, false, SC>(g, first, a, cn, stk, sp); break;
-            }
+            // children at depth D: all leaves, nothing to push
+            if (ent.x >= (3u << BH_NKIDS_SHIFT))
+                bh_group_leaves<4, COUNT, SC>(g, first, a, cn);
+            else if (cnt == 3)
+                bh_group_leaves<3, COUNT, SC>(g, first, a, cn);
+            else if (cnt == 2)
+                bh_group_leaves<2, COUNT, SC>(g, first, a, cn);
+            else
+                bh_group_leaves<1, COUNT, SC>(g, first, a, cn);
         }
         __syncwarp();
     }
