@@ -13,7 +13,7 @@ synthetic data: BASELINE.json configs[3]), on the device
 with inputs resident in HBM.  The timed region covers iterations
 [R+W, R+W+K) of the real 1000-iteration schedule (exaggeration 12 for 250,
 momentum 0.5 -> 0.8).  Setup (synthetic data, kNN graph via torch/cuBLAS,
-perplexity calibration via the CPU oracle, symmetrisation via a torch sort)
+perplexity calibration via the GPU bh_bsp, symmetrisation via a torch sort)
 is identical for both arms and cached in /tmp to spare the second arm.
 
 Prints ONE JSON line on rank 0 (see README of the driver contract): value =
@@ -99,15 +99,15 @@ def symmetrize_torch(indices, cond, dev):
 def problem(config: str, dev):
     """Returns dict(n, row_offsets, col (int32), val (f32), y0 (N,2))."""
     os.makedirs(CACHE, exist_ok=True)
-    path = os.path.join(CACHE, f"{config}_v1.npz")
+    path = os.path.join(CACHE, f"{config}_v2.npz")
     if os.path.exists(path):
         try:
             with np.load(path) as z:
                 return {k: z[k] for k in z.files}
         except Exception:
             pass
+    import paper_2212_11506_b200 as bh
     from paper_2212_11506_b200 import workloads
-    from oracle import oracle as o
     t0 = time.time()
     spec = workloads.CONFIGS[config]
     x = spec["gen"]()
@@ -116,13 +116,15 @@ def problem(config: str, dev):
     idx, sqd = knn_torch(x, 90, dev)
     log(f"[setup] kNN (torch) {time.time() - t0:.1f}s")
     t0 = time.time()
-    o.set_threads(0)
-    betas, cond = o.calibrate_perplexity(sqd, 30.0)
-    log(f"[setup] BSP (oracle) {time.time() - t0:.1f}s")
+    pr = bh.calibrate_perplexity(
+        bh.NeighborGraph(indices=idx, sq_distances=sqd), 30.0)
+    cond = pr.conditional.cpu().numpy()
+    log(f"[setup] BSP (GPU) {time.time() - t0:.1f}s")
     t0 = time.time()
     ro, co, va = symmetrize_torch(idx, cond, dev)
     log(f"[setup] symmetrize (torch) {time.time() - t0:.1f}s nnz={co.shape[0]}")
-    y0 = np.column_stack(o.init_embedding(x.shape[0], 0)).astype(np.float32)
+    # Y0 from Philox(0) as the reference's init_embedding (optimizer.py:147)
+    y0 = bh.init_embedding(x.shape[0], 0).y.cpu().numpy().astype(np.float32)
     out = dict(n=np.array(x.shape[0]), row_offsets=ro, col=co, val=va, y0=y0)
     try:
         np.savez(path + ".tmp.npz", **out)

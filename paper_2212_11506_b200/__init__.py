@@ -16,6 +16,7 @@ from .affinity import (NeighborGraph, PerplexityResult, SparseAffinity,
 from .estimator import BarnesHutTSNE
 from .forces import (GradientBuffers, attractive, repulsive_bh,
                      repulsive_counts, repulsive_exact)
+from .knn import knn_exact
 from .optimizer import (STAGES, Embedding, Engine, StepTimings, TsneConfig,
                         embedding_from, gradient_step, init_embedding,
                         kl_divergence, run)
@@ -31,5 +32,5 @@ __all__ = [
     "attractive", "repulsive_bh", "repulsive_exact", "repulsive_counts",
     "Embedding", "TsneConfig", "StepTimings", "init_embedding",
     "embedding_from", "gradient_step", "kl_divergence", "run", "Engine",
-    "BarnesHutTSNE", "STAGES",
+    "BarnesHutTSNE", "STAGES", "knn_exact",
 ]

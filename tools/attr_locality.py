@@ -32,7 +32,7 @@ def main():
     dev = torch.device("cuda", 0)
     prob = bench.problem(args.config, dev)
     p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
-    cache = f"/tmp/bh_bench_cache/{args.config}_y{args.preroll}.npy"
+    cache = f"/tmp/bh_bench_cache/{args.config}_v2_y{args.preroll}.npy"
     if os.path.exists(cache):
         e = bh.embedding_from(np.load(cache))
         e.iteration = args.preroll

@@ -32,7 +32,7 @@ def child(args):
     dev = torch.device("cuda", 0)
     prob = bench.problem(args.config, dev)
     p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
-    cache = f"/tmp/bh_bench_cache/{args.config}_y{args.preroll}.npy"
+    cache = f"/tmp/bh_bench_cache/{args.config}_v2_y{args.preroll}.npy"
     cfg = bh.TsneConfig(theta=args.theta)
     if os.path.exists(cache):
         y = np.load(cache)
