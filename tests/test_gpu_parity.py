@@ -366,8 +366,8 @@ def test_engine_graph_equals_eager_and_is_deterministic(bh):
     np.testing.assert_array_equal(outs[0], outs[2])
 
 
-@pytest.mark.parametrize("code_bits", [32, 64])
-def test_fused_forces_bitwise_equal_separate(bh, code_bits):
+@pytest.mark.parametrize("code_bits,theta", [(32, 0.5), (64, 0.5), (32, 0.8)])
+def test_fused_forces_bitwise_equal_separate(bh, code_bits, theta):
     """bh_forces (one launch, interleaved traversal and CSR-sweep CTAs) gives
     the bitwise trajectory of the separate attractive + repulsive kernels,
     in the fast path and in the evented path."""
@@ -384,7 +384,8 @@ def test_fused_forces_bitwise_equal_separate(bh, code_bits):
     for fuse, timed in ((True, False), (False, False), (True, True)):
         e = bh.embedding_from(y0)
         cfg = bh.TsneConfig(n_iter=60, exaggeration_iters=20, graph_chunk=10,
-                            code_bits=code_bits, relabel_every=20)
+                            code_bits=code_bits, relabel_every=20,
+                            theta=theta)
         eng = bh.Engine(p, e, cfg)
         eng.fuse = fuse
         eng.fuse_timed = timed
