@@ -1,10 +1,12 @@
 """Benchmark: BH t-SNE gradient iterations/sec at N=1.3M (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c3|c2|c1|c0|c4] [--preroll R]
+                    [--config c3|c2|c1|c0|c4] [--preroll R] [--ncu 0|1]
 
 Defaults (no flags): N=1, W=5, K=995 -- the timed region is the rest of the
-full 1000-iteration run (about 2-3 s of GPU time plus ~1 min of setup).
+full 1000-iteration run (about 2 s of GPU time plus ~1-2 min of setup,
+stage breakdown, ncu child and end-to-end runs).  --gpus N > 1 without
+torchrun re-launches itself under torch.distributed.run (one rank per GPU).
 --config c4 runs the per-kernel microbench of BASELINE.json configs[4].
 
 A step is one gradient iteration (tree build, summarize, attractive,
@@ -13,12 +15,14 @@ synthetic data: BASELINE.json configs[3]), on the device
 with inputs resident in HBM.  The timed region covers iterations
 [R+W, R+W+K) of the real 1000-iteration schedule (exaggeration 12 for 250,
 momentum 0.5 -> 0.8).  Setup (synthetic data, kNN graph via torch/cuBLAS,
-perplexity calibration via the GPU bh_bsp, symmetrisation via a torch sort)
-is identical for both arms and cached in /tmp to spare the second arm.
+perplexity calibration by the C oracle, symmetrisation via a torch sort,
+Y0 from numpy's Philox) is identical for both arms, never touches this
+repo's CUDA library, and is cached in /tmp to spare the second arm.
 
-Prints ONE JSON line on rank 0 (see README of the driver contract): value =
-whole-job iterations/s, e2e = the same through the public host-buffer API,
-roofline of the dominant kernel, cpu_baseline = the CPU oracle (OpenMP
+Prints ONE JSON line on rank 0: value = whole-job iterations/s, e2e = the
+same through the public host-buffer API (the full schedule), roofline of the
+dominant kernel (compulsory bytes / duration, plus the DRAM bytes an ncu
+child of this run measures), cpu_baseline = the CPU oracle (OpenMP
 restatement of the reference) on the host cores.
 """
 
@@ -48,7 +52,11 @@ def log(*a):
 
 
 # ---------------------------------------------------------------------------
-# problem setup (identical for both arms)
+# problem setup (identical for both arms; none of it runs this repo's CUDA
+# library: the kNN graph is torch/cuBLAS, the perplexity calibration is the
+# C oracle (the reference's BSP restated, oracle/bh_oracle.c), the
+# symmetrisation torch ops, Y0 numpy's Philox -- so the reference arm never
+# loads libbhtsne_b200.so)
 # ---------------------------------------------------------------------------
 def knn_torch(x: np.ndarray, k: int, dev):
     """kNN graph for the benchmark inputs (setup only): fp32 distances via
@@ -96,36 +104,53 @@ def symmetrize_torch(indices, cond, dev):
             vals.to(torch.float32).cpu().numpy())
 
 
+def init_y0(n: int, seed: int = 0) -> np.ndarray:
+    """optimizer.py:147-158: Philox(seed) standard normal * 1e-4, f32."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    return (rng.standard_normal((n, 2)) * 1e-4).astype(np.float32)
+
+
+def _workloads():
+    """paper_2212_11506_b200/workloads.py (numpy generators) loaded by path,
+    without importing the package."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "bh_workloads", os.path.join(REPO, "paper_2212_11506_b200",
+                                     "workloads.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def problem(config: str, dev):
     """Returns dict(n, row_offsets, col (int32), val (f32), y0 (N,2))."""
     os.makedirs(CACHE, exist_ok=True)
-    path = os.path.join(CACHE, f"{config}_v2.npz")
+    path = os.path.join(CACHE, f"{config}_v3.npz")
     if os.path.exists(path):
         try:
             with np.load(path) as z:
                 return {k: z[k] for k in z.files}
         except Exception:
             pass
-    import paper_2212_11506_b200 as bh
-    from paper_2212_11506_b200 import workloads
+    from oracle import oracle as o
+    workloads = _workloads()
     t0 = time.time()
     spec = workloads.CONFIGS[config]
     x = spec["gen"]()
     log(f"[setup] {config}: data {x.shape} in {time.time() - t0:.1f}s")
     t0 = time.time()
     idx, sqd = knn_torch(x, 90, dev)
-    log(f"[setup] kNN (torch) {time.time() - t0:.1f}s")
+    log(f"[setup] kNN (torch/cuBLAS) {time.time() - t0:.1f}s")
     t0 = time.time()
-    pr = bh.calibrate_perplexity(
-        bh.NeighborGraph(indices=idx, sq_distances=sqd), 30.0)
-    cond = pr.conditional.cpu().numpy()
-    log(f"[setup] BSP (GPU) {time.time() - t0:.1f}s")
+    o.build()
+    o.set_threads(0)
+    _, cond = o.calibrate_perplexity(sqd, 30.0)
+    log(f"[setup] BSP (C oracle, host) {time.time() - t0:.1f}s")
     t0 = time.time()
     ro, co, va = symmetrize_torch(idx, cond, dev)
     log(f"[setup] symmetrize (torch) {time.time() - t0:.1f}s nnz={co.shape[0]}")
-    # Y0 from Philox(0) as the reference's init_embedding (optimizer.py:147)
-    y0 = bh.init_embedding(x.shape[0], 0).y.cpu().numpy().astype(np.float32)
-    out = dict(n=np.array(x.shape[0]), row_offsets=ro, col=co, val=va, y0=y0)
+    out = dict(n=np.array(x.shape[0]), row_offsets=ro, col=co, val=va,
+               y0=init_y0(x.shape[0], 0))
     try:
         np.savez(path + ".tmp.npz", **out)
         os.replace(path + ".tmp.npz", path)
@@ -191,26 +216,38 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle (reference restatement) timing
 # ---------------------------------------------------------------------------
-def cpu_oracle_time(prob, y, steps, code_bits=32):
-    """Full oracle gradient iterations on the host cores from state y."""
+def cpu_oracle_time(prob, y, it0, steps, warmup=0, code_bits=32):
+    """Full oracle gradient iterations (the reference's algorithm restated in
+    C/OpenMP, oracle/bh_oracle.c) on the host cores from state y at
+    iteration it0, with the run() schedule's exaggeration (x12 below
+    iteration 250) and momentum; `warmup` untimed iterations first."""
     from oracle import oracle as o
     threads = o.set_threads(0)
     n = int(prob["n"])
     s = o.State(np.ascontiguousarray(y[:, 0]), np.ascontiguousarray(y[:, 1]),
                 np.zeros(n, np.float32), np.zeros(n, np.float32),
-                np.ones(n, np.float32), np.ones(n, np.float32), 0)
+                np.ones(n, np.float32), np.ones(n, np.float32), it0)
     ro = prob["row_offsets"]
     co = prob["col"].astype(np.int64)
     va = prob["val"]
+    va12 = va * np.float32(12.0)  # set_exaggeration (affinity.py:161-173)
     stage = np.zeros(5)
     tot = np.zeros(5)
+
+    def step():
+        o.gradient_step(s, ro, co, va12 if s.iteration < 250 else va,
+                        code_bits=code_bits, stage_s=stage)
+
+    for _ in range(warmup):
+        step()
     t0 = time.perf_counter()
     for _ in range(steps):
-        o.gradient_step(s, ro, co, va, code_bits=code_bits, stage_s=stage)
+        step()
         tot += stage
     dt = time.perf_counter() - t0
     return dt, threads, dict(zip(("tree", "summarize", "attractive",
-                                  "repulsive", "update"), (tot / steps).tolist()))
+                                  "repulsive", "update"),
+                                 (tot / max(1, steps)).tolist()))
 
 
 def cpu_model():
@@ -227,31 +264,38 @@ def cpu_model():
 # arms
 # ---------------------------------------------------------------------------
 def reference_arm(args, rank, world):
+    """The reference's CPU implementation of the path on the host cores: the
+    C/OpenMP restatement of bhtsne's gradient_step (the reference itself is
+    Python + numba and cannot travel to the GPU box).  Same config, metric
+    and schedule window as our arm: W untimed iterations from Y0, then K
+    timed ones.  Rank 0 only; this repo's CUDA library is never loaded."""
     if rank != 0:
         return
     import torch
-    dev = torch.device("cuda", 0) if torch.cuda.is_available() else None
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else "cpu"
     prob = problem(args.config, dev)
     n = int(prob["n"])
-    y = prob["y0"]
-    w = min(args.warmup, 1)
-    steps = max(1, min(args.steps, args.ref_max_steps))
-    if w:
-        cpu_oracle_time(prob, y, w)
-    dt, threads, stages = cpu_oracle_time(prob, y, steps)
+    steps = args.steps
+    capped = args.ref_max_steps and steps > args.ref_max_steps
+    if capped:
+        steps = args.ref_max_steps
+    dt, threads, stages = cpu_oracle_time(prob, prob["y0"], 0, steps,
+                                          warmup=args.warmup)
     v = steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "it/s",
-        "n_gpus": world, "steps": steps, "warmup": w,
+        "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic", "config": config_dict(args, n, int(prob["col"].shape[0])),
         "cpu_baseline": {"value": v, "unit": "it/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{steps} full gradient iteration(s) of "
-                                   f"{args.config} from Y0 on {threads} threads "
-                                   f"({cpu_model()}); requested steps capped "
-                                   f"at {args.ref_max_steps}",
+                                   f"{args.config} (iterations [{args.warmup}, "
+                                   f"{args.warmup + steps}) of the schedule from "
+                                   f"Y0) on {threads} threads ({cpu_model()})"
+                                   + (f"; requested {args.steps} steps capped at "
+                                      f"{args.ref_max_steps}" if capped else ""),
                          "stage_s": stages},
         "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -270,7 +314,9 @@ def config_dict(args, n, nnz):
             "timed_iterations": [args.preroll + args.warmup,
                                  args.preroll + args.warmup + args.steps],
             "l2": "inputs larger than L2 (CSR P alone > 126 MB); no flush",
-            "parallelism": f"dp{args.gpus} (points/rows sharded, tree replicated)",
+            "parallelism": f"dp{args.gpus} (storage slots / CSR rows sharded "
+                           "by cost, tree replicated, Z partials all-reduced, "
+                           "Y all-gathered)",
             "stage_breakdown": f"stage_ms/kernels: iterations [{args.preroll + args.warmup + args.steps}, "
                                f"+{args.stage_iters}) with attractive and repulsive "
                                "as separate launches, then "
@@ -279,12 +325,130 @@ def config_dict(args, n, nnz):
             "fused_forces": not args.no_fuse}
 
 
+def kernel_bytes(n, nnz_pad, n_nodes, pt=8):
+    """Compulsory DRAM bytes of one launch (every input read once, every
+    output written once; re-reads served by L1/L2 are not counted).
+    pt = bytes per point (8 in f32).  Attractive: the padded CSR stream
+    (4 B col + 4 B val per entry), row_ptr, y_i, each y_j once, attr out.
+    Traversal: every node record (16 B), the sorted points (leaf points),
+    the query points, rank (4 B), rep out, one Z partial per 128 points."""
+    att = 8.0 * nnz_pad + 8.0 * (n + 1) + 3.0 * pt * n
+    rep = 16.0 * n_nodes + 3.0 * pt * n + 4.0 * n + 8.0 * n / 128.0
+    return att, rep
+
+
+NCU_METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,"
+               "dram__bytes_write.sum,smsp__inst_executed.sum,"
+               "smsp__issue_active.avg.pct_of_peak_sustained_active,"
+               "l1tex__t_sector_hit_rate.pct,lts__t_sector_hit_rate.pct,"
+               "l1tex__throughput.avg.pct_of_peak_sustained_active")
+
+
+def ncu_child(args):
+    """Under ncu (--profile-from-start off): advance the problem to the
+    middle of the parent's timed window with the fast graphs, then profile
+    one eager iteration with the fused force launch over all rows and one
+    with the separate attractive / traversal launches."""
+    import torch
+
+    import paper_2212_11506_b200 as bh
+    torch.cuda.set_device(0)
+    prob = problem(args.config, torch.device("cuda", 0))
+    p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
+    e = bh.embedding_from(prob["y0"])
+    cfg = bh.TsneConfig(theta=args.theta, graph_chunk=args.chunk,
+                        relabel_every=args.relabel_every)
+    eng = bh.Engine(p, e, cfg, schedule=True)
+    eng.run(args.ncu_iteration)
+    eng.attr_split = 0.0
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    eng.run(1, use_graph=False)
+    eng.fuse = False
+    eng.run(1, use_graph=False)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+
+
+def ncu_profile(args):
+    """DRAM bytes, duration and issue activity per kernel of one iteration,
+    measured by ncu on a child of this run (same problem, same build).
+    Returns {kernel: {metric: value}} (first launch of each name per
+    profiled iteration: 'fused' for k_forces) or None."""
+    import csv
+    import shutil
+    exe = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(exe):
+        return None
+    out = os.path.join(CACHE, f"ncu_{os.getpid()}.csv")
+    cmd = [exe, "--profile-from-start", "off", "--clock-control", "none",
+           "--metrics", NCU_METRICS, "--csv", "--log-file", out,
+           sys.executable, os.path.abspath(__file__), "--ncu-child",
+           "--config", args.config, "--theta", str(args.theta),
+           "--ncu-iteration", str(args.ncu_iteration),
+           "--relabel-every", str(args.relabel_every)]
+    t0 = time.time()
+    try:
+        r = subprocess.run(cmd, stdout=subprocess.DEVNULL,
+                           stderr=subprocess.PIPE, timeout=args.ncu_timeout,
+                           text=True)
+    except (subprocess.TimeoutExpired, OSError) as exc:
+        log(f"[ncu] skipped: {exc}")
+        return None
+    log(f"[ncu] rc={r.returncode} in {time.time() - t0:.0f}s")
+    if r.returncode != 0 or not os.path.exists(out):
+        log(r.stderr[-2000:])
+        return None
+    rows = []
+    with open(out) as fh:
+        lines = [ln for ln in fh if ln.startswith('"')]
+    for rec in csv.DictReader(lines):
+        rows.append(rec)
+    launches = {}
+    for rec in rows:
+        key = (int(rec["ID"]), rec["Kernel Name"])
+        try:
+            val = float(rec["Metric Value"].replace(",", ""))
+        except ValueError:
+            continue
+        launches.setdefault(key, {})[rec["Metric Name"]] = val
+    table = []
+    for (lid, name), m in sorted(launches.items()):
+        short = name.split("(")[0].replace("void ", "").split("<")[0]
+        short = short.replace("bh::", "")
+        table.append(dict(id=lid, kernel=short, **m))
+    try:
+        os.remove(out)
+    except OSError:
+        pass
+    return table
+
+
+def summarize_ncu(table):
+    """Per-kernel view of the ncu table: the fused k_forces launch, the
+    separate k_attractive (rows [0, n)) and k_repulsive launches, and the
+    whole profiled fused iteration."""
+    if not table:
+        return None
+    res = {}
+    fused_seen = False
+    for row in table:
+        k = row["kernel"]
+        if k == "k_forces" and not fused_seen:
+            res["forces"] = row
+            fused_seen = True
+        elif k == "k_attractive" and fused_seen and "attractive" not in res:
+            res["attractive"] = row
+        elif k == "k_repulsive" and fused_seen and "repulsive" not in res:
+            res["repulsive"] = row
+    return res
+
+
 def ours_arm(args, rank, world):
     import torch
     import torch.distributed as dist
 
     import paper_2212_11506_b200 as bh
-    from paper_2212_11506_b200 import _lib
 
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -305,7 +469,6 @@ def ours_arm(args, rank, world):
         from paper_2212_11506_b200.dist import Shard
         shard = Shard(rank, world)
     eng = bh.Engine(p, e, cfg, schedule=True, shard=shard)
-    eng.overlap = args.overlap
     eng.fuse = not args.no_fuse
     eng.chunk_graph = args.chunk_graph
     if args.attr_split is not None:
@@ -330,33 +493,32 @@ def ours_arm(args, rank, world):
     torch.cuda.synchronize()
     ms = start.elapsed_time(stop)
     launches = eng.launches - launches0
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     # --- per-stage breakdown: the next stage_iters iterations with the
-    #     evented graphs and the kernels back to back (isolated durations;
-    #     outside the timed region, where the CSR sweep overlaps the chain)
-    timings = bh.StepTimings()
-    eng.overlap = False
+    #     evented graphs (outside the timed region): separate kernels over
+    #     all rows (isolated durations), the fused launch over all rows (the
+    #     roofline's kernel), then the timed region's pipeline
+    split = eng.attr_split
+    timings, timings_f, timings_p = bh.StepTimings(), bh.StepTimings(), bh.StepTimings()
+    eng.attr_split = 0.0
+    fuse = eng.fuse
+    eng.fuse = False
     eng.run(args.stage_iters, timings)
-    timings_f = bh.StepTimings()
-    timings_p = bh.StepTimings()
-    if eng.fuse and world == 1:
-        # the fused force launch on its own (all rows), evented: the kernel
-        # of the roofline; then the timed region's pipeline (side-stream
-        # sweep + fused launch sharing the rows), evented: "forces" is the
-        # force phase from the end of summarize to the join
+    eng.fuse = fuse
+    if eng.fuse:
         eng.fuse_timed = True
-        split = eng.attr_split
-        eng.attr_split = 0.0
         eng.run(args.stage_iters, timings_f)
         eng.attr_split = split
         if split:
             eng.run(args.stage_iters, timings_p)
         eng.fuse_timed = False
-    eng.overlap = args.overlap
-    y_start = e.y.cpu().numpy() if rank == 0 else None
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    eng.attr_split = split
+    lo_ = eng.tree.level_off.cpu().numpy()
+    n_nodes = int(lo_[int(lo_[-1])])
+    nnz_pad = int(eng.rp[-1].item())
     y_end = e.y.cpu().numpy() if rank == 0 else None
     if rank != 0:
         return
@@ -371,85 +533,105 @@ def ours_arm(args, rank, world):
         if timings_p.calls(s_):
             stage_ms[key] = 1e3 * timings_p.total(s_) / timings_p.calls(s_)
 
-    # --- roofline: algorithmic bytes per launch / launch time
+    # --- roofline of the dominant kernel (the fused force launch)
+    peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        peak = float(json.load(open(peaks_path))["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        peak, peak_src = FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+    pt = 16 if args.precision == "f64" else 8
+    att_b, rep_b = kernel_bytes(n, nnz_pad, n_nodes, pt)
+    if args.precision == "f64":
+        att_b += 4.0 * nnz_pad  # f64 values
+        rep_b += 16.0 * n_nodes
+    # the SURVEY 8(d) logical bytes: every visited record / leaf point
+    # counted per visit (served by L1/L2 after the first touch)
     counts = []
-    for ysnap in (y_start, y_end):
+    for ysnap in (y_end,):
         c, r = bh.compute_bounds(ysnap)
         t = bh.summarize(bh.build_tree(bh.morton_codes(ysnap, c, r), ysnap))
         cnt = bh.repulsive_counts(t, args.theta).astype(np.int64)
         counts.append(cnt.sum(axis=0))
         del t
     cnt = np.mean(counts, axis=0)
-    # 16 B per node record visited (internal + leaf), 8 B per leaf point,
-    # 28 B per point (y_i, order, rep out, z) -- SURVEY.md 8(d)
-    # (f64 run precision: 32 B records, 16 B points, 8 B values)
-    w = 2.0 if args.precision == "f64" else 1.0
-    rep_bytes = 16.0 * w * (cnt[0] + cnt[1]) + 8.0 * w * cnt[2] + (
-        28.0 + 16.0 * (w - 1.0)) * n
-    att_bytes = (4.0 + 4.0 * w) * nnz + 4.0 * (n + 1) + 16.0 * w * n
-    peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
-    try:
-        peak = float(json.load(open(peaks_path))["hbm_gbs"])
-        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        peak, peak_src = FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+    logical_rep = 16.0 * (cnt[0] + cnt[1]) + 8.0 * cnt[2] + 28.0 * n
     kernels = {}
-    for name, b in (("repulsive", rep_bytes), ("attractive", att_bytes)):
+    for name, b in (("repulsive", rep_b), ("attractive", att_b)):
         t_ms = stage_ms[name]
-        ach = b / (t_ms * 1e-3) / 1e9
-        kernels[name] = {"ms": t_ms, "algorithmic_bytes": b,
-                         "achieved_gbs": ach, "frac": ach / peak}
+        kernels[name] = {"ms": t_ms, "compulsory_bytes": b,
+                         "achieved_gbs": b / (t_ms * 1e-3) / 1e9,
+                         "frac": b / (t_ms * 1e-3) / 1e9 / peak}
+    kernels["repulsive"]["logical_bytes_incl_cache_hits"] = logical_rep
+    kernels["repulsive"]["logical_gbs_incl_cache_hits"] = (
+        logical_rep / (stage_ms["repulsive"] * 1e-3) / 1e9)
+    dom = "repulsive"
     if stage_ms.get("forces"):
-        # the fused force launch (all rows + the traversal), launched on its
-        # own; in the timed region a side-stream sweep launch takes rows
-        # [0, split) under the tree build and the fused launch the rest
-        b = rep_bytes + att_bytes
-        ach = b / (stage_ms["forces"] * 1e-3) / 1e9
-        kernels["forces"] = {"ms": stage_ms["forces"], "algorithmic_bytes": b,
-                             "achieved_gbs": ach, "frac": ach / peak,
-                             "fused": ["attractive", "repulsive"]}
+        b = rep_b + att_b
+        kernels["forces"] = {"ms": stage_ms["forces"], "compulsory_bytes": b,
+                             "achieved_gbs": b / (stage_ms["forces"] * 1e-3) / 1e9,
+                             "frac": b / (stage_ms["forces"] * 1e-3) / 1e9 / peak,
+                             "fused": ["attractive", "repulsive"],
+                             "logical_bytes_incl_cache_hits": logical_rep + att_b}
         if stage_ms.get("force_phase_pipelined"):
             kernels["forces"]["timed_region_force_phase_ms"] = stage_ms[
                 "force_phase_pipelined"]
-    dom = max(kernels, key=lambda k: kernels[k]["ms"])
-    traffic = None
-    ncu_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(ncu_path):
-        try:
-            tr = json.load(open(ncu_path)).get(args.config, {}).get(dom)
-            traffic = None if tr is None else float(tr)
-        except Exception:
-            traffic = None
+        dom = "forces"
+    ncu = None
+    if args.ncu and world == 1:
+        ncu = summarize_ncu(ncu_profile(args))
+    if ncu:
+        for name, row in ncu.items():
+            if name in kernels:
+                tr = row.get("dram__bytes_read.sum", 0.0) + row.get(
+                    "dram__bytes_write.sum", 0.0)
+                dur = row.get("gpu__time_duration.sum", float("nan")) * 1e-9
+                kernels[name]["ncu"] = {
+                    "dram_bytes": tr, "duration_ms": dur * 1e3,
+                    "dram_gbs": tr / dur / 1e9,
+                    "dram_frac": tr / dur / 1e9 / peak,
+                    "issue_active_pct": row.get(
+                        "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "warp_instructions": row.get("smsp__inst_executed.sum"),
+                    "l1_hit_pct": row.get("l1tex__t_sector_hit_rate.pct"),
+                    "l2_hit_pct": row.get("lts__t_sector_hit_rate.pct"),
+                    "l1tex_throughput_pct": row.get(
+                        "l1tex__throughput.avg.pct_of_peak_sustained_active")}
+    kd = kernels[dom]
     roof = {"bound": "hbm", "kernel": dom,
-            "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
-            "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
+            "achieved": kd["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": kd["frac"],
+            "traffic": kd["ncu"]["dram_bytes"] if "ncu" in kd else None,
             "peak_source": peak_src,
-            # the north star's nominal ~8 TB/s, for reference
-            "peak_nominal": 8000.0,
-            "frac_nominal": kernels[dom]["achieved_gbs"] / 8000.0,
+            "bytes": "compulsory (each CSR entry, node record, point read "
+                     "once; outputs written once) per launch over all rows "
+                     "and points, / the launch's evented duration",
+            "traffic_source": ("ncu dram__bytes_read+write.sum of the same "
+                               "launch (child of this run, iteration "
+                               f"{args.ncu_iteration})") if "ncu" in kd else None,
+            "limiter": "issue (traversal CTAs) + L1TEX wavefronts of the "
+                       "y_j gathers (sweep CTAs); see kernels.*.ncu",
             "visits_per_point": (cnt[0] + cnt[1]) / n,
             "leaf_points_per_point": cnt[2] / n}
 
-    # --- e2e through the public host-buffer API (per step: pinned host
-    #     embedding state -> device, one iteration, state -> pinned host)
+    # --- e2e through the public API with host buffers
     runs = [e2e_run(bh, prob, cfg, args) for _ in range(max(1, args.e2e_repeats))]
     vals = sorted(r["value"] for r in runs)
-    e2e = dict(runs[0], value=vals[len(vals) // 2],
+    e2e = dict(runs[len(runs) // 2], value=vals[len(vals) // 2],
                repeats=[r["value"] for r in runs],
-               breakdowns=[r["breakdown_s"] for r in runs],
-               clocks_per_run=[r["clocks"] for r in runs],
                summary=f"median of {len(runs)} end-to-end runs")
     e2e["per_step_host_state"] = e2e_host(bh, p, cfg, y_end, args)
 
     # --- CPU oracle on the host cores, bounded sample from the same state
     cpu = None
     if args.cpu_steps > 0:
-        dt, threads, stages = cpu_oracle_time(prob, y_end, args.cpu_steps)
+        it0 = args.preroll + args.warmup + args.steps + 3 * args.stage_iters
+        dt, threads, stages = cpu_oracle_time(prob, y_end, it0, args.cpu_steps)
         cpu = {"value": args.cpu_steps / dt, "unit": "it/s", "cores": threads,
                "kind": "port",
                "sample": f"{args.cpu_steps} full gradient iteration(s) of "
-                         f"{args.config} (N={n}) from the Y at the end of the "
-                         f"timed region, C/OpenMP oracle on {threads} threads "
+                         f"{args.config} (N={n}) from the Y after the timed "
+                         f"region, C/OpenMP oracle on {threads} threads "
                          f"({cpu_model()})",
                "stage_s": stages}
     line = {
@@ -467,17 +649,18 @@ def ours_arm(args, rank, world):
 
 
 def e2e_run(bh, prob, cfg, args):
-    """End to end through the public optimiser API with HOST inputs: the
-    symmetric P (CSR) and Y0 in pinned host memory are uploaded, the engine
-    is built (row padding, graph capture) and runs the same W+K schedule
-    iterations, and the final embedding is read back -- all inside the
-    host-wall-clock timed region.  it/s = K / (time * K / (W + K))."""
+    """End to end through the public optimiser API with HOST inputs, the
+    way a user runs it: the symmetric P (CSR) and Y0 in pinned host memory
+    are uploaded, the engine is built (row padding, graph capture) and runs
+    the whole n_iter-iteration schedule (its non-finite check and Z read
+    back every graph_chunk iterations), and the final embedding is read
+    back -- all inside the host-wall-clock timed region.
+    it/s = n_iter / time."""
     import torch
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     ro, co, va = pin(prob["row_offsets"]), pin(prob["col"]), pin(prob["val"])
     y0 = pin(prob["y0"])
-    iters = args.warmup + args.steps
-    # release the previous run's engine before timing this one
+    iters = cfg.n_iter
     import gc
     gc.collect()
     torch.cuda.synchronize()
@@ -499,11 +682,15 @@ def e2e_run(bh, prob, cfg, args):
         dt = tick() - t0
     h2d = sum(int(t.numel() * t.element_size()) for t in (ro, co, va, y0))
     d2h = int(y_out.numel() * y_out.element_size())
+    sched = 96 * math.ceil(iters / cfg.graph_chunk)
     return {"value": iters / dt, "unit": "it/s",
-            "h2d_bytes_per_step": h2d / iters, "d2h_bytes_per_step": d2h / iters,
+            "h2d_bytes_per_step": h2d / iters,
+            "d2h_bytes_per_step": (d2h + sched) / iters,
             "api": f"Engine(from_csr(host P), embedding_from(host Y0)).run({iters}) "
                    "+ Y to host; pinned host buffers; host wall clock incl. "
-                   "upload, CSR padding, CUDA-graph capture and readback",
+                   "upload, CSR padding, relabels, CUDA-graph capture and "
+                   "readback (the full schedule: run()'s loop, "
+                   "optimizer.py:316-325)",
             "steps": iters,
             "breakdown_s": {"upload": t1 - t0, "engine_init": t2 - t1,
                             "run": t3 - t2, "readback": t0 + dt - t3},
@@ -511,6 +698,8 @@ def e2e_run(bh, prob, cfg, args):
 
 
 def e2e_host(bh, p, cfg, y_host, args):
+    """gradient_step-style use: the embedding state lives on the host and
+    every step uploads it, runs one iteration and reads it back."""
     import torch
     n = y_host.shape[0]
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
@@ -536,11 +725,11 @@ def e2e_host(bh, p, cfg, y_host, args):
         one()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    bytes_state = 3 * n * 2 * 4
+    bytes_state = 3 * n * 2 * y_host.dtype.itemsize
     return {"value": steps / dt, "unit": "it/s",
             "h2d_bytes_per_step": bytes_state, "d2h_bytes_per_step": bytes_state,
             "api": "Engine.run(1) per step on host-resident (y, v, g): pinned "
-                   "H2D, one graph-free iteration incl. bounds/centering, "
+                   "H2D, one graph iteration incl. bounds/centering, "
                    "D2H; host wall clock", "steps": steps}
 
 
@@ -596,7 +785,7 @@ def c4_arm(args, rank, world):
     import paper_2212_11506_b200 as bh
     from paper_2212_11506_b200 import _lib
     from paper_2212_11506_b200._lib import call, ptr, stream
-    from paper_2212_11506_b200.dist import ShardPlan
+    from paper_2212_11506_b200.dist import equal_share
 
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -606,8 +795,8 @@ def c4_arm(args, rank, world):
     torch.cuda.synchronize()
     log(f"[setup] c4 N={y.shape[0]} nnz={p.nnz} in {time.time() - t0:.1f}s")
     n, nnz = y.shape[0], p.nnz
-    plan = ShardPlan(n, world, rank)
-    lo, hi = plan.mine
+    eq = equal_share(n, world)
+    lo, hi = min(n, rank * eq), min(n, (rank + 1) * eq)
     yt = torch.from_numpy(y).to(dev)
     c, r = bh.compute_bounds(yt)
     tree = bh.summarize(bh.build_tree(bh.morton_codes(yt, c, r), yt))
@@ -684,9 +873,10 @@ def main():
     ap.add_argument("--chunk", type=int, default=25)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=50)
-    ap.add_argument("--e2e-repeats", type=int, default=5,
+    ap.add_argument("--e2e-repeats", type=int, default=3,
                     help="end-to-end runs through the public API (median)")
-    ap.add_argument("--ref-max-steps", type=int, default=3)
+    ap.add_argument("--ref-max-steps", type=int, default=200,
+                    help="cap of the reference arm's timed steps (0: none)")
     ap.add_argument("--relabel-every", type=int, default=50,
                     help="Morton relabeling period of the engine (0: never)")
     ap.add_argument("--attr-split", type=float, default=None,
@@ -696,17 +886,35 @@ def main():
     ap.add_argument("--no-fuse", action="store_true",
                     help="separate attractive/repulsive launches in the "
                          "timed region (A/B of the fused force pass)")
-    ap.add_argument("--overlap", action="store_true",
-                    help="CSR sweep on a side stream under the chain (A/B test)")
     ap.add_argument("--stage-iters", type=int, default=50,
                     help="iterations after the timed region measured with "
                          "per-stage events (kernel breakdown / roofline)")
+    ap.add_argument("--ncu", type=int, default=1,
+                    help="1: measure the dominant kernel's DRAM bytes with "
+                         "an ncu child of this run (N=1 only)")
+    ap.add_argument("--ncu-iteration", type=int, default=500,
+                    help="schedule iteration the ncu child profiles")
+    ap.add_argument("--ncu-timeout", type=float, default=300.0)
+    ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ncu_child:
+        ncu_child(args)
+        return
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(29500 + os.getpid() % 1000),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        log("[bench] spawning " + " ".join(cmd[2:6]) + " ...")
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch
         import torch.distributed as dist

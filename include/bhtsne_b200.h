@@ -90,6 +90,17 @@ typedef struct bh_sched_t {
     double learning_rate_f64, min_gain_f64;
 } bh_sched_t;
 
+/* The engine's share of the work, resident on the device so
+ * that captured CUDA graphs stay valid when bh_partition re-balances it.
+ * Storage slots / CSR rows [lo, hi) belong to this rank (lo is a multiple of
+ * BH_REP_POINTS_PER_PARTIAL); rows [lo, split) are swept by
+ * bh_step_attractive (a side stream, under the tree build), rows
+ * [split, hi) inside bh_step_forces.  One GPU: lo = 0, hi = n. */
+typedef struct bh_part_t {
+    int64_t lo, hi, split;
+    int64_t world;
+} bh_part_t;
+
 /* Node record of the level-contiguous quadtree (16 bytes):
  *   x, y  : centre of mass (float32, quadtree.py:488-508)
  *   mass  : point count (float32 value; exact below 2^24 points)
@@ -302,6 +313,96 @@ int bh_update_f64(double *y, double *v, double *g, const double *attr,
                   void *ws, size_t ws_bytes, bh_stream_t stream);
 int bh_center_f64(double *y, int64_t n, const bh_bounds_t *bounds,
                   bh_stream_t stream);
+
+/* ---- the optimiser loop's engine entry points ------------------------------
+ * gradient_step (optimizer.py:195-224) and the run() loop (optimizer.py:
+ * 316-325) as the engine runs them: points live in "storage slots" (the
+ * Morton order of the last relabel), one GPU -- or each of several -- owns
+ * the slots and CSR rows of its bh_part_t (device-resident; bh_partition).
+ *
+ * bh_partition: balanced cuts of [0, n) for `world` GPUs at multiples of
+ *   BH_REP_POINTS_PER_PARTIAL (cost of a slot: w_point + its row length),
+ *   cuts (world + 1, device int64) and parts[world] (device); rows
+ *   [lo, lo + split_frac (hi - lo)) are the side sweep's.  Equal shares when
+ *   a balanced range would exceed cap slots.
+ * bh_step_attractive: forces.py:56-82 over rows [lo, split) of *part (the
+ *   side-stream sweep that overlaps the tree build).
+ * bh_step_qlist: the share's slots in the current sorted order (the
+ *   entries of tree order[] inside [lo, hi), stable) -- several GPUs only.
+ * bh_step_forces: mode 0 = one launch, the traversal of the share's points
+ *   in the current Morton order (forces.py:85-150; qlist, or all of
+ *   tree->order on one GPU (qlist = NULL); query y[slot], self = its sorted
+ *   position rank[slot]; writes rep[slot] and zpart[slot]) interleaved with
+ *   the sweep of rows [split, hi); mode 1 = the traversal alone, mode 2 =
+ *   the sweep alone (bitwise the same results as mode 0).  ws:
+ *   bh_repulsive_workspace_bytes(max_points); max_points bounds hi - lo.
+ * bh_step_zsum: zblock[b] = the fixed-order sum of zpart over the share's
+ *   128-slot blocks b (the same blocks and sums on any number of GPUs);
+ *   z_out (optional, one GPU): their fixed-order total (sched->z).
+ * bh_step_update: the update (bh_update) of slots [lo, hi); reduce = 1 (one
+ *   GPU, [lo, hi) = [0, n)) also finishes the iteration (mean, bounds of
+ *   the re-centred cloud, iteration + 1), else bh_step_finish does that
+ *   after the y exchange, bitwise the same.  ysend (optional): the new y of
+ *   the share, packed from row 0.
+ * bh_pack_rows / bh_unpack_rows: dst[i] = src[lo + i] for the share; and
+ *   dst[cuts[r] + j] = gbuf[r * cap + j] (an all-gather of packed shares
+ *   with `cap` rows per rank back into slot order). */
+int bh_partition(const int64_t *row_ptr, int64_t n, int world, double w_point,
+                 double split_frac, int64_t cap, int64_t *cuts,
+                 bh_part_t *parts, bh_stream_t stream);
+int bh_step_attractive(const int64_t *row_ptr, const int32_t *col,
+                       const float *val, int padded, const float *y,
+                       const bh_part_t *part, int64_t max_rows,
+                       const bh_sched_t *sched, float *attr,
+                       bh_stream_t stream);
+size_t bh_step_qlist_workspace_bytes(int64_t n);
+int bh_step_qlist(const int32_t *order, int64_t n, const bh_part_t *part,
+                  int32_t *qlist, void *ws, size_t ws_bytes,
+                  bh_stream_t stream);
+int bh_step_forces(const bh_tree_t *tree, const bh_bounds_t *bounds,
+                   double theta, const float *y, const int32_t *rank,
+                   const int32_t *qlist, const bh_part_t *part,
+                   int64_t max_points, int mode, float *rep, double *zpart,
+                   void *ws, size_t ws_bytes, const int64_t *row_ptr,
+                   const int32_t *col, const float *val, int padded,
+                   const bh_sched_t *sched, float *attr, bh_stream_t stream);
+size_t bh_step_zsum_workspace_bytes(int64_t n);
+int bh_step_zsum(const double *zpart, const bh_part_t *part, int64_t n,
+                 int64_t max_points, double *zblock, double *z_out, void *ws,
+                 size_t ws_bytes, bh_stream_t stream);
+int bh_step_update(float *y, float *v, float *g, const float *attr,
+                   const float *rep, const bh_part_t *part, int64_t n,
+                   bh_sched_t *sched, bh_bounds_t *bounds_out, int code_bits,
+                   int reduce, float *ysend, void *ws, size_t ws_bytes,
+                   bh_stream_t stream);
+int bh_step_finish(const float *y, int64_t n, bh_sched_t *sched,
+                   bh_bounds_t *bounds_out, int code_bits, void *ws,
+                   size_t ws_bytes, bh_stream_t stream);
+int bh_step_attractive_f64(const int64_t *row_ptr, const int32_t *col,
+                           const double *val, int padded, const double *y,
+                           const bh_part_t *part, int64_t max_rows,
+                           const bh_sched_t *sched, double *attr,
+                           bh_stream_t stream);
+int bh_step_forces_f64(const bh_tree_t *tree, const bh_bounds_t *bounds,
+                       double theta, const double *y, const int32_t *rank,
+                       const int32_t *qlist, const bh_part_t *part,
+                       int64_t max_points, int mode, double *rep,
+                       double *zpart, void *ws, size_t ws_bytes,
+                       const int64_t *row_ptr, const int32_t *col,
+                       const double *val, int padded, const bh_sched_t *sched,
+                       double *attr, bh_stream_t stream);
+int bh_step_update_f64(double *y, double *v, double *g, const double *attr,
+                       const double *rep, const bh_part_t *part, int64_t n,
+                       bh_sched_t *sched, bh_bounds_t *bounds_out,
+                       int code_bits, int reduce, double *ysend, void *ws,
+                       size_t ws_bytes, bh_stream_t stream);
+int bh_step_finish_f64(const double *y, int64_t n, bh_sched_t *sched,
+                       bh_bounds_t *bounds_out, int code_bits, void *ws,
+                       size_t ws_bytes, bh_stream_t stream);
+int bh_pack_rows(const void *src, const bh_part_t *part, int64_t cap,
+                 int elem_bytes, void *dst, bh_stream_t stream);
+int bh_unpack_rows(const void *gbuf, int64_t cap, const int64_t *cuts,
+                   int world, int elem_bytes, void *dst, bh_stream_t stream);
 
 /* ---- binary-search perplexity: calibrate_perplexity (affinity.py:61-118) --
  * One warp per row, f64 bisection with the reference's exact schedule. */

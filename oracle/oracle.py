@@ -242,9 +242,10 @@ def tree_dump(t: OracleTree) -> str:
 
 # --- forces (forces.py) -----------------------------------------------------
 
-def attractive(row_offsets, col_indices, values, y):
+def attractive(row_offsets, col_indices, values, y, n_rows=None):
+    """forces.py:56-82; rows [0, n_rows) (default: one per point)."""
     y0, y1 = split_xy(y)
-    n = y0.shape[0]
+    n = y0.shape[0] if n_rows is None else int(n_rows)
     a0 = np.empty(n, np.float32)
     a1 = np.empty(n, np.float32)
     lib().or_attractive(np.ascontiguousarray(row_offsets, np.int64),

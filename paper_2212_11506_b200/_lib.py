@@ -131,6 +131,31 @@ SIGNATURES = {
     "bh_gather_rows": ([_P, _P, _I64, C.c_int, _P, _P], C.c_int),
     "bh_scatter_rows": ([_P, _P, _I64, C.c_int, _P, _P], C.c_int),
     "bh_invert_perm": ([_P, _I64, _P, _P], C.c_int),
+    "bh_partition": ([_P, _I64, C.c_int, C.c_double, C.c_double, _I64, _P,
+                      _P, _P], C.c_int),
+    "bh_step_attractive": ([_P, _P, _P, C.c_int, _P, _P, _I64, _P, _P, _P],
+                           C.c_int),
+    "bh_step_attractive_f64": ([_P, _P, _P, C.c_int, _P, _P, _I64, _P, _P,
+                                _P], C.c_int),
+    "bh_step_forces": ([C.POINTER(TreeStruct), _P, C.c_double, _P, _P, _P,
+                        _P, _I64, C.c_int, _P, _P, _P, _SZ, _P, _P, _P,
+                        C.c_int, _P, _P, _P], C.c_int),
+    "bh_step_forces_f64": ([C.POINTER(TreeStruct), _P, C.c_double, _P, _P,
+                            _P, _P, _I64, C.c_int, _P, _P, _P, _SZ, _P, _P,
+                            _P, C.c_int, _P, _P, _P], C.c_int),
+    "bh_step_qlist_workspace_bytes": ([_I64], _SZ),
+    "bh_step_qlist": ([_P, _I64, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_step_zsum_workspace_bytes": ([_I64], _SZ),
+    "bh_step_zsum": ([_P, _P, _I64, _I64, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_step_update": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P, C.c_int,
+                        C.c_int, _P, _P, _SZ, _P], C.c_int),
+    "bh_step_update_f64": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P, C.c_int,
+                            C.c_int, _P, _P, _SZ, _P], C.c_int),
+    "bh_step_finish": ([_P, _I64, _P, _P, C.c_int, _P, _SZ, _P], C.c_int),
+    "bh_step_finish_f64": ([_P, _I64, _P, _P, C.c_int, _P, _SZ, _P],
+                           C.c_int),
+    "bh_pack_rows": ([_P, _P, _I64, C.c_int, _P, _P], C.c_int),
+    "bh_unpack_rows": ([_P, _I64, _P, C.c_int, C.c_int, _P, _P], C.c_int),
     "bh_permute_csr_workspace_bytes": ([_I64], _SZ),
     "bh_permute_csr": ([_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _SZ, _P],
                        C.c_int),

@@ -221,6 +221,14 @@ struct RepArgs {
     double *__restrict__ zblock;
     unsigned *__restrict__ ticket;
     double *__restrict__ z_out;
+    // engine mode (part != NULL): the share's hi - lo storage slots, taken
+    // in the current Morton order -- qlist[i] (several GPUs: the share's
+    // slots in sorted order, bh_step_qlist) or order[i] (one GPU: all of
+    // them); coordinates y_query[slot] (ys[i] on one GPU), self = its sorted
+    // position (rank[slot]); rep[slot] and zpart[slot]
+    const bh_part_t *__restrict__ part;
+    const int32_t *__restrict__ rank;
+    const int32_t *__restrict__ qlist;
 };
 
 // Self correction (SC): when theta <= kScTheta no point accepts an
@@ -261,14 +269,30 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
     double *__restrict__ zblock = A.zblock;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool slots = A.part != nullptr;
+    const int64_t lo = slots ? 0 : t_begin;
+    const int64_t hi = slots ? A.part->hi - A.part->lo : t_end;
+    if (lo + bid * kRepThreads >= hi) return;  // engine mode: past the share
     if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-    const int64_t t = t_begin + (bid * kRepWarps + warp) * 32 + lane;
-    const bool valid = t < t_end && *status == BH_OK;
+    const int64_t t = lo + (bid * kRepWarps + warp) * 32 + lane;
+    const bool valid = t < hi && *status == BH_OK;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     float2 yi = make_float2(0.f, 0.f);
-    if (valid) yi = QUERY ? A.y_query[order[t]] : ys[t];
-    const uint32_t self = (uint32_t)t;
+    uint32_t self = (uint32_t)t;
+    int64_t slot = 0;
+    if (valid) {
+        if (slots && A.qlist) {
+            slot = A.qlist[t];
+            yi = A.y_query[slot];
+            if (!SC) self = (uint32_t)A.rank[slot];
+        } else if (slots) {
+            slot = order[t];
+            yi = ys[t];
+        } else {
+            yi = QUERY ? A.y_query[order[t]] : ys[t];
+        }
+    }
     double r0 = 0.0, r1 = 0.0, z = 0.0;
     RepCounts cn = {0, 0, 0, 0};
     uint4 *stk = s_stack[warp];
@@ -330,13 +354,17 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
 
     if (SC && valid) z -= 1.0;  // the self leaf's exact +1 (kScTheta)
     if (valid) {
-        const int64_t o = A.sorted_out ? t - t_begin : (int64_t)order[t];
+        const int64_t o = slots ? slot
+                                : (A.sorted_out ? t - t_begin : (int64_t)order[t]);
         A.rep[o] = make_float2((float)r0, (float)r1);
         if (A.zpart) A.zpart[o] = z;
         if (COUNT) A.counts[o] = make_int4(cn.internal, cn.leafnodes, cn.leafpts, cn.accepted);
     }
-    rep_z_tail(z, warp, lane, bid, nblk, s_z, &s_done, zblock, A.ticket,
-               A.z_out);
+    // engine mode: Z from zpart[slot] by slot blocks (bh_step_zsum), the
+    // same sums for any number of GPUs
+    if (!slots)
+        rep_z_tail(z, warp, lane, bid, nblk, s_z, &s_done, zblock, A.ticket,
+                   A.z_out);
 }
 
 template <int D, bool COUNT, bool QUERY, bool SC>
@@ -368,6 +396,9 @@ struct AttArgs {
     float exag_param;
     const bh_sched_t *__restrict__ sched;
     float2 *__restrict__ attr;
+    // engine mode (part != NULL): the rows of att_rows (forces.cuh)
+    const bh_part_t *__restrict__ part;
+    int which;
 };
 
 // CTA `bid` of `nblk` sweeping CTAs of THREADS threads: row batches of
@@ -381,14 +412,15 @@ __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
     const int32_t *__restrict__ col = A.col;
     const float *__restrict__ val = A.val;
     const float2 *__restrict__ y = A.y;
-    const int64_t row_end = A.row_end;
+    int64_t row_begin, row_end;
+    att_rows(A, row_begin, row_end);
     const bh_sched_t *__restrict__ sched = A.sched;
     const float exag = sched ? (sched->iteration < sched->exaggeration_iters
                                     ? sched->exaggeration
                                     : 1.0f)
                              : A.exag_param;
     const int gl = threadIdx.x % G;
-    for (int64_t r0 = A.row_begin + bid * kRows; r0 < row_end;
+    for (int64_t r0 = row_begin + bid * kRows; r0 < row_end;
          r0 += nblk * kRows) {
     const int64_t row = r0 + threadIdx.x / G;
     const bool ok = row < row_end;
@@ -833,4 +865,114 @@ extern "C" int bh_kl_rows_f64(const int64_t *row_ptr, const int32_t *col,
                               void *ws, size_t ws_bytes, bh_stream_t stream) {
     (void)padded;
     return kl_impl(row_ptr, col, val, n, y, z, kl_out, ws, ws_bytes, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Engine entry points (the share of bh_part_t; storage-slot traversal).
+// ---------------------------------------------------------------------------
+namespace bh {
+static int fuse_na(int64_t nr, int64_t rows, int rows_per_cta) {
+    static const double ratio = [] {
+        const char *s = getenv("BH_FUSE_RATIO");
+        const double r = s ? atof(s) : 2.0;
+        return r > 0.0 ? r : 2.0;
+    }();
+    return (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)ceil((double)nr / ratio),
+                             bh_blocks(rows, rows_per_cta)));
+}
+}  // namespace bh
+
+extern "C" int bh_step_attractive(const int64_t *row_ptr, const int32_t *col,
+                                  const float *val, int padded, const float *y,
+                                  const bh_part_t *part, int64_t max_rows,
+                                  const bh_sched_t *sched, float *attr,
+                                  bh_stream_t stream) {
+    BH_REQUIRE(part && sched, "part and sched are required");
+    if (max_rows <= 0) return BH_OK;
+    constexpr int G = 16;
+    const AttArgs A{row_ptr, col, val, (const float2 *)y, 0, 0, 1.0f, sched,
+                    (float2 *)attr, part, 0};
+    const int grid = bh_blocks(max_rows, kAttThreads / G);
+    if (padded)
+        BH_LAUNCH("k_attractive", (k_attractive<G, true>), grid, kAttThreads,
+                  0, bh_cs(stream), A);
+    else
+        BH_LAUNCH("k_attractive", (k_attractive<G, false>), grid, kAttThreads,
+                  0, bh_cs(stream), A);
+    BH_CHECK_LAUNCH("k_attractive");
+    return BH_OK;
+}
+
+extern "C" int bh_step_forces(const bh_tree_t *t, const bh_bounds_t *bounds,
+                              double theta, const float *y,
+                              const int32_t *rank, const int32_t *qlist,
+                              const bh_part_t *part, int64_t max_points,
+                              int mode, float *rep, double *zpart, void *ws,
+                              size_t ws_bytes, const int64_t *row_ptr,
+                              const int32_t *col, const float *val,
+                              int padded, const bh_sched_t *sched,
+                              float *attr, bh_stream_t stream) {
+    BH_REQUIRE(theta >= 0, "theta must be >= 0, got %g", theta);
+    BH_REQUIRE(t->precision != 64, "precision-64 tree: use the _f64 entry point");
+    BH_REQUIRE(part && y && rank && zpart && sched,
+               "part, y, rank, zpart and sched are required");
+    BH_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (fused), 1 or 2");
+    BH_REQUIRE(max_points >= 1 && max_points <= t->n_points,
+               "bad max_points");
+    BH_REQUIRE(ws_bytes >= bh_repulsive_workspace_bytes(max_points),
+               "repulsive workspace too small");
+    constexpr int G = 16;
+    const int64_t nr = rep_grid(max_points);
+    unsigned *ticket = (unsigned *)((char *)ws + bh_align(sizeof(double) * nr));
+    const RepArgs R{(const float4 *)t->node, (const float2 *)t->ys, t->order,
+                    (const float2 *)y, bounds, t->status, theta, 0,
+                    t->n_points, 0, (float2 *)rep, zpart, nullptr, nullptr,
+                    ticket, nullptr, part, rank, qlist};
+    const AttArgs A{row_ptr, col, val, (const float2 *)y, 0, 0, 1.0f, sched,
+                    (float2 *)attr, part, 1};
+    const bool sc = theta <= kScTheta;
+    cudaStream_t st = bh_cs(stream);
+    if (mode == 2) {  // the sweep of rows [split, hi) alone
+        const int grid = bh_blocks(max_points, kAttThreads / G);
+        if (padded)
+            BH_LAUNCH("k_attractive", (k_attractive<G, true>), grid,
+                      kAttThreads, 0, st, A);
+        else
+            BH_LAUNCH("k_attractive", (k_attractive<G, false>), grid,
+                      kAttThreads, 0, st, A);
+        BH_CHECK_LAUNCH("k_attractive");
+        return BH_OK;
+    }
+#define BH_STEP_REP(D, SC)                                                    \
+    BH_LAUNCH("k_repulsive", (k_repulsive<D, false, false, SC>), (int)nr,     \
+              kRepThreads, 0, st, R)
+#define BH_STEP_FUSED(D, SC)                                                  \
+    {                                                                         \
+        const int64_t na = fuse_na(nr, max_points, kRepThreads / G);          \
+        if (padded)                                                           \
+            BH_LAUNCH("k_forces", (k_forces<D, G, true, SC>),                 \
+                      (unsigned)(nr + na), kRepThreads, 0, st, R, A, nr, na); \
+        else                                                                  \
+            BH_LAUNCH("k_forces", (k_forces<D, G, false, SC>),                \
+                      (unsigned)(nr + na), kRepThreads, 0, st, R, A, nr, na); \
+    }
+#define BH_STEP(D)                                                            \
+    if (mode == 1) {                                                          \
+        if (sc) BH_STEP_REP(D, true); else BH_STEP_REP(D, false);             \
+    } else {                                                                  \
+        if (sc) BH_STEP_FUSED(D, true) else BH_STEP_FUSED(D, false)           \
+    }
+    if (t->code_bits == 32) {
+        BH_STEP(16)
+    } else if (t->code_bits == 64) {
+        BH_STEP(32)
+    } else {
+        return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
+    }
+#undef BH_STEP
+#undef BH_STEP_FUSED
+#undef BH_STEP_REP
+    BH_CHECK_LAUNCH("k_forces");
+    return BH_OK;
 }

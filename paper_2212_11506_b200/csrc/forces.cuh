@@ -28,6 +28,20 @@ __device__ __forceinline__ double fixed_sum(const double *x, int64_t n) {
     return warp_sum(s);
 }
 
+// The row range of a CSR sweep: explicit, or the engine's share (bh_part_t):
+// rows [part->lo, part->split) when which == 0 (the side-stream sweep),
+// [part->split, part->hi) otherwise.
+template <typename Args>
+__device__ __forceinline__ void att_rows(const Args &A, int64_t &b, int64_t &e) {
+    if (A.part) {
+        b = A.which ? A.part->split : A.part->lo;
+        e = A.which ? A.part->hi : A.part->split;
+    } else {
+        b = A.row_begin;
+        e = A.row_end;
+    }
+}
+
 struct RepCounts {
     int internal, leafnodes, leafpts, accepted;
 };
@@ -80,8 +94,10 @@ struct Acc64 {
 // independent of the GPU count.  No CTA-wide barrier: the
 // last warp of the CTA to finish folds the warp partials.  s_z has
 // kRepWarps entries; *s_done starts at 0.
+// zidx: this CTA's partial slot (its block index, or slot / 128 in the
+// engine's slot mode); nblk: the CTAs that write partials [0, nblk).
 __device__ __forceinline__ void rep_z_tail(double z, int warp, int lane,
-                                           int64_t bid, int64_t nblk,
+                                           int64_t zidx, int64_t nblk,
                                            double *s_z, unsigned *s_done,
                                            double *zblock, unsigned *ticket,
                                            double *z_out) {
@@ -98,7 +114,7 @@ __device__ __forceinline__ void rep_z_tail(double z, int warp, int lane,
         double bz = 0.0;
         for (int w = 0; w < kRepWarps; w++)
             bz = __dadd_rn(bz, ((volatile double *)s_z)[w]);
-        zblock[bid] = bz;
+        zblock[zidx] = bz;
         if (z_out) {
             __threadfence();
             last = atomicAdd(ticket, 1u) == (unsigned)(nblk - 1);

@@ -124,6 +124,9 @@ struct RepArgs64 {
     double *__restrict__ zblock;
     unsigned *__restrict__ ticket;
     double *__restrict__ z_out;
+    const bh_part_t *__restrict__ part;  // engine mode (forces.cu RepArgs)
+    const int32_t *__restrict__ rank;
+    const int32_t *__restrict__ qlist;
 };
 
 __device__ __forceinline__ uint4 side2_entry(uint32_t info, uint32_t msk,
@@ -141,13 +144,30 @@ __device__ __forceinline__ void rep_block64(const RepArgs64 &A, int64_t bid,
     __shared__ double s_z[kRepWarps];
     __shared__ unsigned s_done;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool slots = A.part != nullptr;
+    const int64_t lo = slots ? 0 : A.t_begin;
+    const int64_t hi = slots ? A.part->hi - A.part->lo : A.t_end;
+    if (lo + bid * kRepThreads >= hi) return;  // engine mode: past the share
     if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-    const int64_t t = A.t_begin + (bid * kRepWarps + warp) * 32 + lane;
-    const bool valid = t < A.t_end && *A.status == BH_OK;
+    const int64_t t = lo + (bid * kRepWarps + warp) * 32 + lane;
+    const bool valid = t < hi && *A.status == BH_OK;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     double2 yi = make_double2(0.0, 0.0);
-    if (valid) yi = QUERY ? A.y_query[A.order[t]] : A.ys[t];
+    uint32_t self = (uint32_t)t;
+    int64_t slot = 0;
+    if (valid) {
+        if (slots && A.qlist) {
+            slot = A.qlist[t];
+            yi = A.y_query[slot];
+            self = (uint32_t)A.rank[slot];
+        } else if (slots) {
+            slot = A.order[t];
+            yi = A.ys[t];
+        } else {
+            yi = QUERY ? A.y_query[A.order[t]] : A.ys[t];
+        }
+    }
     const double theta2 = __dmul_rn(A.theta, A.theta);
     Acc64 a{0.0, 0.0, 0.0};
     RepCounts cn = {0, 0, 0, 0};
@@ -171,7 +191,7 @@ __device__ __forceinline__ void rep_block64(const RepArgs64 &A, int64_t bid,
         const double side2 = __longlong_as_double(
             (long long)(((unsigned long long)ent.w << 32) | ent.z));
         const Ctx64 g{A.node, A.ys, yi, side2, theta2, ((ent.y >> lane) & 1u) != 0,
-                      (uint32_t)t, lane};
+                      self, lane};
         uint32_t info = 0, msk = 0;
         // straight-line code per (warp-uniform) child count, every record of
         // the group loaded up front; full groups tested first on the raw word
@@ -194,13 +214,15 @@ __device__ __forceinline__ void rep_block64(const RepArgs64 &A, int64_t bid,
         __syncwarp();
     }
     if (valid) {
-        const int64_t o = A.sorted_out ? t - A.t_begin : (int64_t)A.order[t];
+        const int64_t o = slots ? slot
+                                : (A.sorted_out ? t - A.t_begin : (int64_t)A.order[t]);
         A.rep[o] = make_double2(a.r0, a.r1);
         if (A.zpart) A.zpart[o] = a.z;
         if (COUNT) A.counts[o] = make_int4(cn.internal, cn.leafnodes, cn.leafpts, cn.accepted);
     }
-    rep_z_tail(a.z, warp, lane, bid, nblk, s_z, &s_done, A.zblock, A.ticket,
-               A.z_out);
+    if (!slots)  // engine mode: bh_step_zsum
+        rep_z_tail(a.z, warp, lane, bid, nblk, s_z, &s_done, A.zblock,
+                   A.ticket, A.z_out);
 }
 
 template <int D, bool COUNT, bool QUERY>
@@ -220,6 +242,8 @@ struct AttArgs64 {
     double exag_param;
     const bh_sched_t *__restrict__ sched;
     double2 *__restrict__ attr;
+    const bh_part_t *__restrict__ part;  // engine mode (att_rows, forces.cuh)
+    int which;
 };
 
 // Attractive sweep CTA `bid` of `nblk` (THREADS threads), G lanes per row
@@ -232,14 +256,15 @@ __device__ __forceinline__ void att_block64(const AttArgs64 &A, int64_t bid,
     const int32_t *__restrict__ col = A.col;
     const double *__restrict__ val = A.val;
     const double2 *__restrict__ y = A.y;
-    const int64_t row_end = A.row_end;
+    int64_t row_begin, row_end;
+    att_rows(A, row_begin, row_end);
     const bh_sched_t *__restrict__ sched = A.sched;
     const double exag = sched ? (sched->iteration < sched->exaggeration_iters
                                      ? sched->exaggeration_f64
                                      : 1.0)
                               : A.exag_param;
     const int gl = threadIdx.x % G;
-    for (int64_t r0 = A.row_begin + bid * kRows; r0 < row_end;
+    for (int64_t r0 = row_begin + bid * kRows; r0 < row_end;
          r0 += nblk * kRows) {
         const int64_t row = r0 + threadIdx.x / G;
         const bool ok = row < row_end;
@@ -495,5 +520,94 @@ extern "C" int bh_repulsive_exact_f64(const double *y, int64_t n, double *rep,
         (const double2 *)y, n, (double2 *)rep, zpart, (double *)w,
         (unsigned *)(w + bh_align(sizeof(double) * grid)), z_out);
     BH_CHECK_LAUNCH("k_repulsive_exact64");
+    return BH_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Engine entry points in f64 (bh_step_attractive / bh_step_forces, forces.cu).
+// ---------------------------------------------------------------------------
+extern "C" int bh_step_attractive_f64(const int64_t *row_ptr,
+                                      const int32_t *col, const double *val,
+                                      int padded, const double *y,
+                                      const bh_part_t *part, int64_t max_rows,
+                                      const bh_sched_t *sched, double *attr,
+                                      bh_stream_t stream) {
+    BH_REQUIRE(part && sched, "part and sched are required");
+    if (max_rows <= 0) return BH_OK;
+    constexpr int G = 16;
+    const AttArgs64 A{row_ptr, col, val, (const double2 *)y, 0, 0, 1.0, sched,
+                      (double2 *)attr, part, 0};
+    const int grid = bh_blocks(max_rows, 256 / G);
+    if (padded)
+        BH_LAUNCH("k_attractive64", (k_attractive64<G, true>), grid, 256, 0,
+                  bh_cs(stream), A);
+    else
+        BH_LAUNCH("k_attractive64", (k_attractive64<G, false>), grid, 256, 0,
+                  bh_cs(stream), A);
+    BH_CHECK_LAUNCH("k_attractive64");
+    return BH_OK;
+}
+
+extern "C" int bh_step_forces_f64(const bh_tree_t *t,
+                                  const bh_bounds_t *bounds, double theta,
+                                  const double *y, const int32_t *rank,
+                                  const int32_t *qlist, const bh_part_t *part,
+                                  int64_t max_points, int mode, double *rep,
+                                  double *zpart, void *ws, size_t ws_bytes,
+                                  const int64_t *row_ptr, const int32_t *col,
+                                  const double *val, int padded,
+                                  const bh_sched_t *sched, double *attr,
+                                  bh_stream_t stream) {
+    BH_REQUIRE(theta >= 0, "theta must be >= 0, got %g", theta);
+    BH_REQUIRE(t->precision == 64, "bh_step_forces_f64 needs a precision-64 tree");
+    BH_REQUIRE(part && y && rank && zpart && sched,
+               "part, y, rank, zpart and sched are required");
+    BH_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (fused), 1 or 2");
+    BH_REQUIRE(max_points >= 1 && max_points <= t->n_points,
+               "bad max_points");
+    BH_REQUIRE(ws_bytes >= bh_repulsive_workspace_bytes(max_points),
+               "repulsive workspace too small");
+    constexpr int G = 16;
+    const int64_t nr = rep_grid(max_points);
+    unsigned *ticket = (unsigned *)((char *)ws + bh_align(sizeof(double) * nr));
+    const RepArgs64 R{(const void *)t->node, (const double2 *)t->ys, t->order,
+                      (const double2 *)y, bounds, t->status, theta, 0,
+                      t->n_points, 0, (double2 *)rep, zpart, nullptr,
+                      nullptr, ticket, nullptr, part, rank, qlist};
+    const AttArgs64 A{row_ptr, col, val, (const double2 *)y, 0, 0, 1.0, sched,
+                      (double2 *)attr, part, 1};
+    cudaStream_t st = bh_cs(stream);
+    if (mode == 2) {
+        const int grid = bh_blocks(max_points, 256 / G);
+        if (padded)
+            BH_LAUNCH("k_attractive64", (k_attractive64<G, true>), grid, 256,
+                      0, st, A);
+        else
+            BH_LAUNCH("k_attractive64", (k_attractive64<G, false>), grid, 256,
+                      0, st, A);
+        BH_CHECK_LAUNCH("k_attractive64");
+        return BH_OK;
+    }
+    const int64_t na = std::max<int64_t>(
+        1, std::min<int64_t>((nr + 1) / 2, bh_blocks(max_points, kRepThreads / G)));
+#define BH_STEP64(D)                                                          \
+    if (mode == 1)                                                            \
+        BH_LAUNCH("k_repulsive64", (k_repulsive64<D, false, false>), (int)nr, \
+                  kRepThreads, 0, st, R);                                     \
+    else if (padded)                                                          \
+        BH_LAUNCH("k_forces64", (k_forces64<D, G, true>), (unsigned)(nr + na),\
+                  kRepThreads, 0, st, R, A, nr, na);                          \
+    else                                                                      \
+        BH_LAUNCH("k_forces64", (k_forces64<D, G, false>),                    \
+                  (unsigned)(nr + na), kRepThreads, 0, st, R, A, nr, na);
+    if (t->code_bits == 32) {
+        BH_STEP64(16)
+    } else if (t->code_bits == 64) {
+        BH_STEP64(32)
+    } else {
+        return set_error(BH_ERR_UNSUPPORTED, "code_bits must be 32 or 64");
+    }
+#undef BH_STEP64
+    BH_CHECK_LAUNCH("k_forces64");
     return BH_OK;
 }

@@ -322,13 +322,44 @@ using sched_t = typename std::conditional<std::is_same<T, float>::value,
 __device__ __forceinline__ float fsub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double fsub_rn(double a, double b) { return __dsub_rn(a, b); }
 
+// The last block of k_update / k_finish: y -= T(mean_f64(y))
+// (optimizer.py:220-221) is published as the pending shift; rounding is
+// monotone, so min(y - m) == rn(min(y) - m) and the bounds of the re-centred
+// cloud come straight from the extrema.  Advances the iteration.
+template <typename T>
+__device__ void finish_iteration(const PtPartial<T> *part, int nparts,
+                                 int64_t n, int it, int code_bits,
+                                 bh_sched_t *sched, bh_bounds_t *out,
+                                 unsigned *ticket) {
+    PtPartial<T> r = reduce_partials(part, nparts);
+    if (threadIdx.x == 0) {
+        const double d0 = __ddiv_rn(r.s0, (double)n);
+        const double d1 = __ddiv_rn(r.s1, (double)n);
+        const T m0 = (T)d0, m1 = (T)d1;
+        finalize_bounds(fsub_rn(r.mn0, m0), fsub_rn(r.mx0, m0),
+                        fsub_rn(r.mn1, m1), fsub_rn(r.mx1, m1), r.bad,
+                        code_bits, (float)m0, (float)m1, (double)m0,
+                        (double)m1, out);
+        sched->iteration = it + 1;
+        *ticket = 0;
+    }
+}
+
+// The update of slots [lo, hi) (all n points, or the engine's share `pr`).
+// reduce: also reduce the new y (extrema and f64 sums, grid-stride order
+// over [0, n)) and finish the iteration -- one GPU, where [lo, hi) = [0, n).
+// Otherwise (several GPUs) k_finish does that after the y exchange, over
+// the same grid in the same order, so the mean and the bounds are bitwise
+// those of one GPU.  ysend (optional): the new y of the share, packed from 0.
 template <typename T>
 __global__ void __launch_bounds__(kPtThreads)
 k_update(p2_t<T> *__restrict__ y, p2_t<T> *__restrict__ v,
          p2_t<T> *__restrict__ g, const p2_t<T> *__restrict__ attr,
          const p2_t<T> *__restrict__ rep, const int32_t *__restrict__ rep_rank,
          int64_t n, bh_sched_t *sched, bh_bounds_t *out, int code_bits,
-         PtPartial<T> *part, unsigned *ticket) {
+         PtPartial<T> *part, unsigned *ticket,
+         const bh_part_t *__restrict__ pr, p2_t<T> *__restrict__ ysend,
+         int reduce) {
     bh_pdl_trigger();  // the successor may launch early (PDL)
     bh_pdl_wait();     // the predecessor's results are visible
 
@@ -338,8 +369,9 @@ k_update(p2_t<T> *__restrict__ y, p2_t<T> *__restrict__ v,
     MinMax<T> m;
     mm_init(m);
     double s0 = 0.0, s1 = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = pr ? pr->lo : 0, hi = pr ? pr->hi : n;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+         i < hi; i += (int64_t)gridDim.x * blockDim.x) {
         const p2_t<T> a = attr[i], r = rep[rep_rank ? (int64_t)rep_rank[i] : i];
         // grad = 4.0 * (attr - rep / z)   (optimizer.py:205-207)
         const T gx = S.grad(a.x, r.x), gy = S.grad(a.y, r.y);
@@ -353,27 +385,39 @@ k_update(p2_t<T> *__restrict__ y, p2_t<T> *__restrict__ v,
         y[i] = yy;
         v[i] = vv;
         g[i] = gg;
+        if (ysend) ysend[i - lo] = yy;
+        mm_add(m, yy.x, yy.y);
+        s0 = __dadd_rn(s0, (double)yy.x);
+        s1 = __dadd_rn(s1, (double)yy.y);
+    }
+    if (!reduce) return;
+    block_reduce(m, s0, s1, &part[blockIdx.x]);
+    if (!last_block(ticket)) return;
+    finish_iteration(part, gridDim.x, n, it, code_bits, sched, out, ticket);
+}
+
+// The reduction half of k_update over the exchanged y (several GPUs).
+template <typename T>
+__global__ void __launch_bounds__(kPtThreads)
+k_finish(const p2_t<T> *__restrict__ y, int64_t n, bh_sched_t *sched,
+         bh_bounds_t *out, int code_bits, PtPartial<T> *part,
+         unsigned *ticket) {
+    bh_pdl_trigger();
+    bh_pdl_wait();
+    const int it = sched->iteration;
+    MinMax<T> m;
+    mm_init(m);
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const p2_t<T> yy = y[i];
         mm_add(m, yy.x, yy.y);
         s0 = __dadd_rn(s0, (double)yy.x);
         s1 = __dadd_rn(s1, (double)yy.y);
     }
     block_reduce(m, s0, s1, &part[blockIdx.x]);
     if (!last_block(ticket)) return;
-    PtPartial<T> r = reduce_partials(part, gridDim.x);
-    if (threadIdx.x == 0) {
-        // y -= T(mean_f64(y))   (optimizer.py:220-221); rounding is
-        // monotone, so min(y - m) == rn(min(y) - m): the bounds of the
-        // re-centred cloud come straight from the extrema.
-        const double d0 = __ddiv_rn(r.s0, (double)n);
-        const double d1 = __ddiv_rn(r.s1, (double)n);
-        const T m0 = (T)d0, m1 = (T)d1;
-        finalize_bounds(fsub_rn(r.mn0, m0), fsub_rn(r.mx0, m0),
-                        fsub_rn(r.mn1, m1), fsub_rn(r.mx1, m1), r.bad,
-                        code_bits, (float)m0, (float)m1, (double)m0,
-                        (double)m1, out);
-        sched->iteration = it + 1;
-        *ticket = 0;
-    }
+    finish_iteration(part, gridDim.x, n, it, code_bits, sched, out, ticket);
 }
 
 template <typename T>
@@ -444,7 +488,43 @@ static int update_impl(T *y, T *v, T *g, const T *attr, const T *rep,
     BH_LAUNCH("k_update", k_update<T>, grid, kPtThreads, 0, bh_cs(stream),
               (p2_t<T> *)y, (p2_t<T> *)v, (p2_t<T> *)g, (const p2_t<T> *)attr,
               (const p2_t<T> *)rep, rep_rank, n, sched, bounds_out, code_bits,
-              part, ticket);
+              part, ticket, (const bh_part_t *)nullptr, (p2_t<T> *)nullptr, 1);
+    return BH_OK;
+}
+
+template <typename T>
+static int step_update_impl(T *y, T *v, T *g, const T *attr, const T *rep,
+                            const bh_part_t *pr, int64_t n, bh_sched_t *sched,
+                            bh_bounds_t *bounds_out, int code_bits,
+                            int reduce, T *ysend, void *ws, size_t ws_bytes,
+                            bh_stream_t stream) {
+    BH_REQUIRE(n >= 1, "need at least one point");
+    BH_REQUIRE(ws_bytes >= pt_ws_bytes(n), "update workspace too small");
+    int grid = pt_grid(n);
+    char *w = (char *)ws;
+    PtPartial<T> *part = (PtPartial<T> *)w;
+    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial<T>) * grid));
+    BH_LAUNCH("k_update", k_update<T>, grid, kPtThreads, 0, bh_cs(stream),
+              (p2_t<T> *)y, (p2_t<T> *)v, (p2_t<T> *)g, (const p2_t<T> *)attr,
+              (const p2_t<T> *)rep, (const int32_t *)nullptr, n, sched,
+              bounds_out, code_bits, part, ticket, pr, (p2_t<T> *)ysend,
+              reduce);
+    return BH_OK;
+}
+
+template <typename T>
+static int step_finish_impl(const T *y, int64_t n, bh_sched_t *sched,
+                            bh_bounds_t *bounds_out, int code_bits, void *ws,
+                            size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(n >= 1, "need at least one point");
+    BH_REQUIRE(ws_bytes >= pt_ws_bytes(n), "update workspace too small");
+    int grid = pt_grid(n);
+    char *w = (char *)ws;
+    PtPartial<T> *part = (PtPartial<T> *)w;
+    unsigned *ticket = (unsigned *)(w + bh_align(sizeof(PtPartial<T>) * grid));
+    BH_LAUNCH("k_finish", k_finish<T>, grid, kPtThreads, 0, bh_cs(stream),
+              (const p2_t<T> *)y, n, sched, bounds_out, code_bits, part,
+              ticket);
     return BH_OK;
 }
 
@@ -496,6 +576,42 @@ extern "C" int bh_update_f64(double *y, double *v, double *g,
                              bh_stream_t stream) {
     return update_impl(y, v, g, attr, rep, rep_rank, n, sched, bounds_out,
                        code_bits, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_step_update(float *y, float *v, float *g, const float *attr,
+                              const float *rep, const bh_part_t *part,
+                              int64_t n, bh_sched_t *sched,
+                              bh_bounds_t *bounds_out, int code_bits,
+                              int reduce, float *ysend, void *ws,
+                              size_t ws_bytes, bh_stream_t stream) {
+    return step_update_impl(y, v, g, attr, rep, part, n, sched, bounds_out,
+                            code_bits, reduce, ysend, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_step_update_f64(double *y, double *v, double *g,
+                                  const double *attr, const double *rep,
+                                  const bh_part_t *part, int64_t n,
+                                  bh_sched_t *sched, bh_bounds_t *bounds_out,
+                                  int code_bits, int reduce, double *ysend,
+                                  void *ws, size_t ws_bytes,
+                                  bh_stream_t stream) {
+    return step_update_impl(y, v, g, attr, rep, part, n, sched, bounds_out,
+                            code_bits, reduce, ysend, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_step_finish(const float *y, int64_t n, bh_sched_t *sched,
+                              bh_bounds_t *bounds_out, int code_bits,
+                              void *ws, size_t ws_bytes, bh_stream_t stream) {
+    return step_finish_impl(y, n, sched, bounds_out, code_bits, ws, ws_bytes,
+                            stream);
+}
+
+extern "C" int bh_step_finish_f64(const double *y, int64_t n,
+                                  bh_sched_t *sched, bh_bounds_t *bounds_out,
+                                  int code_bits, void *ws, size_t ws_bytes,
+                                  bh_stream_t stream) {
+    return step_finish_impl(y, n, sched, bounds_out, code_bits, ws, ws_bytes,
+                            stream);
 }
 
 extern "C" int bh_center(float *y, int64_t n, const bh_bounds_t *bounds,

@@ -28,7 +28,7 @@ from __future__ import annotations
 import math
 import os
 import time
-from dataclasses import dataclass, field, replace
+from dataclasses import astuple, dataclass, field, replace
 
 import numpy as np
 import torch
@@ -196,52 +196,58 @@ def embedding_from(y, v=None, g=None, iteration=0, dtype=None) -> Embedding:
 
 # ---------------------------------------------------------------------------
 # Engine: every buffer of the loop preallocated in HBM; one iteration = one
-# Morton pass, the radix-sort passes, 3 tree kernels, one summarize kernel
-# per level, attractive, repulsive and update, enqueued on the current
-# stream and captured in CUDA graphs.  The state is kept in a private
-# "storage order" that is periodically renumbered to the current Morton
-# order (relabel): CSR rows, their column gathers, the traversal's reads and
-# writes then touch nearby memory.  Results are returned in point-id order.
+# Morton pass, the radix-sort passes, 3 tree kernels, the summarize kernels,
+# the force pass (the side-stream CSR sweep + one fused launch), the update,
+# enqueued on the current stream and captured in CUDA graphs.  The state is
+# kept in a private "storage order", renumbered to the current Morton order
+# before the first iteration and every relabel_every iterations: CSR rows,
+# their column gathers and the traversal's reads and writes then touch
+# nearby memory.  Results are returned in point-id order.
+#
+# The work is the slots / CSR rows of a bh_part_t share (device-resident):
+# all of [0, n) on one GPU; on G GPUs (dist.Shard) a cost-balanced
+# contiguous range per rank, with the tree rebuilt redundantly from the full
+# Y, the Z partials all-reduced and the updated Y all-gathered every
+# iteration.
 # ---------------------------------------------------------------------------
+PART_ALIGN = 128  # BH_REP_POINTS_PER_PARTIAL: one Z partial per 128 slots
+# cost of a point relative to one CSR entry when balancing shares: the
+# traversal (0.97 ms for 1.3M points) against the sweep (0.52 ms for 187M
+# entries) at C3 -> ~270 entries per point
+W_POINT = 270.0
+
+
+def _align(x: int, a: int = PART_ALIGN) -> int:
+    return (x + a - 1) // a * a
+
+
 class Engine:
     # events: 0 start | 1 tree built | 2 summarized | 3 attractive done |
-    #         4 repulsive done | 5 forces joined / exchanged | 6 updated |
-    #         7 attractive start (side stream)
-    N_EVENTS = 8
+    #         4 forces done | 5 Z exchanged | 6 iteration done |
+    #         7 attractive start | 8 update done (before the Y exchange) |
+    #         9 traversal start (separate kernels)
+    N_EVENTS = 10
     STAGE_EVENTS = {"tree": (0, 1), "summarize": (1, 2), "attractive": (7, 3),
-                    "repulsive": (2, 4), "update": (5, 6)}
-    STAGE_EVENTS_SHARDED = {"tree": (0, 1), "summarize": (1, 2),
-                            "attractive": (2, 3), "repulsive": (3, 4),
-                            "update": (5, 6)}
-    STAGE_EVENTS_SEQ = {"tree": (0, 1), "summarize": (1, 2),
-                        "attractive": (7, 3), "repulsive": (3, 4),
-                        "update": (5, 6)}
-
+                    "repulsive": (9, 4), "update": (5, 8)}
     STAGE_EVENTS_FUSED = {"tree": (0, 1), "summarize": (1, 2),
-                          "forces": (2, 4), "update": (5, 6)}
+                          "forces": (2, 4), "update": (5, 8)}
     # with the split sweep: "attractive" = the side-stream launch (concurrent
     # with the tree build), "forces" = end of summarize to the join
     STAGE_EVENTS_FUSED_SPLIT = dict(STAGE_EVENTS_FUSED, attractive=(7, 3))
 
     def _fused(self, timed: bool) -> bool:
-        return (self.shard is None and self.fuse and not self.overlap
-                and (not timed or self.fuse_timed))
-
-    def split_rows(self) -> int:
-        """CSR rows [0, split) swept on the side stream in the fused path."""
-        return int(self.n * self.attr_split)
+        return self.fuse and (not timed or self.fuse_timed)
 
     def fn(self, name: str) -> str:
         """Library entry point in the run precision."""
         return name + "_f64" if self.f64 else name
 
     def _stage_events(self):
-        if self.shard is not None:
-            return self.STAGE_EVENTS_SHARDED
         if self._fused(True):
-            return (self.STAGE_EVENTS_FUSED_SPLIT if self.split_rows()
+            return (self.STAGE_EVENTS_FUSED_SPLIT if self._split_on()
                     else self.STAGE_EVENTS_FUSED)
-        return self.STAGE_EVENTS if self.overlap else self.STAGE_EVENTS_SEQ
+        return (self.STAGE_EVENTS if not self._split_on()
+                else dict(self.STAGE_EVENTS, attractive=(7, 3)))
 
     def __init__(self, p: SparseAffinity, e: Embedding, cfg: TsneConfig,
                  schedule: bool = True, shard=None):
@@ -265,7 +271,8 @@ class Engine:
         # storage-order state (ids[s] = point id stored at slot s)
         self.y, self.v, self.g, self.tmp = f2(), f2(), f2(), f2()
         self.ids = torch.arange(n, dtype=torch.int32, device=dev)
-        self.ids_tmp, self.rank = i32(), i32()
+        self.ids_tmp, self.perm_inv = i32(), i32()
+        self.rank_of = i32()  # slot -> sorted position (tree build)
         rp, col, val = p.padded()
         self.csr = {"p": (rp, col, val.to(dt))}
         self.csr_key = "p"
@@ -289,15 +296,22 @@ class Engine:
             n, dtype=torch.int32 if self.code_bits == 32 else torch.int64,
             device=dev)
         self.tree = TreeArrays(n, self.code_bits, dev, dtype=dt)
+        self.tree.struct.rank = self.rank_of.data_ptr()
         self.ws_sort = _lib.workspace(lib.bh_sort_workspace_bytes(n, self.code_bits))
         self.ws_rep = _lib.workspace(lib.bh_repulsive_workspace_bytes(n))
         self.ws_upd = _lib.workspace(lib.bh_update_workspace_bytes(n))
         self.ws_bnd = _lib.workspace(lib.bh_bounds_workspace_bytes(n))
         self.ws_perm = None
         self.z_dev = self.sched[48:56].view(torch.float64)  # sched.z
+        self.n_zblocks = (n + PART_ALIGN - 1) // PART_ALIGN
+        self.zblock = torch.zeros(self.n_zblocks, dtype=torch.float64,
+                                  device=dev)
+        self.zpart = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.ws_zsum = _lib.workspace(lib.bh_step_zsum_workspace_bytes(n))
         self.theta = float(cfg.theta)
         self.relabel_every = cfg.relabel_every if schedule else 0
         self.since_relabel = 0
+        self.relabeled = False
         self.graphs = {}
         # the iteration chain runs (and is captured) on a high-priority
         # stream; the CSR sweep on a low-priority side stream fills the SMs
@@ -305,30 +319,11 @@ class Engine:
         lo, hi = torch.cuda.Stream.priority_range()
         self.main = torch.cuda.Stream(device=dev, priority=hi)
         self.side = torch.cuda.Stream(device=dev, priority=lo)
-        # True: the CSR sweep runs on the side stream under the chain
-        # (measured +0.6% at C3, profiles/README.md); off by default so the
-        # cooperative summarize launch never contends for SM slots
-        self.overlap = False
-        # fraction of the CSR rows swept on the (low-priority) side stream
-        # under the latency-bound tree build in the fused fast path; the rest
-        # run inside the fused force launch.  Measured at C3 (it/s): 0: 487,
-        # 0.3: 498, 0.4: 505, 0.45: 506, 0.6: 499, 1.0: 479 (round-1 v10);
-        # after the traversal rework and the 10-CTA fused pass: 0.2: 612,
-        # 0.25: 614, 0.3: 619, 0.35: 620, 0.4: 618, 0.45: 613, 0.55: 602
-        self.attr_split = 0.35
-        # f32 runs summarize from the f64 prefix sums of the sorted points
-        # (2 launches; internal centres of mass differ from the reference's
-        # child-order sums by f64 rounding only); f64 runs keep the
-        # bit-exact level-by-level summarize.  The stage API's summarize()
-        # is always the bit-exact one.
-        self.prefix_summary = self.dtype == torch.float32
-        # fuse: the untimed fast path launches the fused force pass
-        # (bh_forces); the evented (StepTimings) path keeps the two kernels
-        # apart for the per-stage breakdown unless fuse_timed is set
+        # fuse: the fast path launches the fused force pass (bh_step_forces
+        # mode 0); the evented (StepTimings) path keeps the two kernels apart
+        # for the per-stage breakdown unless fuse_timed is set
         self.fuse = True
         self.fuse_timed = False
-        # sharded fast path: attractive + its all-gather on the side stream
-        self.shard_overlap = True
         self.launches = 0  # library kernels enqueued by run() (bench claim)
         # True: full chunks of the fast path replay one graph_chunk-iteration
         # graph (+0.2% device time, but capturing 25-iteration graphs for the
@@ -336,9 +331,53 @@ class Engine:
         self.chunk_graph = False
         self.fork_ev = torch.cuda.Event()
         self.join_ev = torch.cuda.Event()
+        # the share of this GPU (bh_part_t rows of `parts`, cuts = the
+        # world + 1 boundaries); one GPU: [0, n)
         self.shard = shard
+        self.world = shard.world if shard is not None else 1
+        self.rank = shard.rank if shard is not None else 0
+        from .dist import share_cap
+        self.cap = share_cap(n, self.world)
+        self.qlist = (torch.zeros(self.cap, dtype=torch.int32, device=dev)
+                      if shard is not None else None)
+        self.ws_q = (_lib.workspace(lib.bh_step_qlist_workspace_bytes(n))
+                     if shard is not None else None)
+        self.cuts = torch.zeros(self.world + 1, dtype=torch.int64, device=dev)
+        self.parts = torch.zeros((self.world, 4), dtype=torch.int64, device=dev)
+        self.part = self.parts[self.rank]
+        # fraction of the share's CSR rows swept on the (low-priority) side
+        # stream under the latency-bound tree build; the rest run inside the
+        # fused force launch.  Measured at C3 (it/s, round 1): 0: 487, 0.2:
+        # 612, 0.25: 614, 0.3: 619, 0.35: 620, 0.4: 618, 0.45: 613, 0.55: 602
+        self._attr_split = 0.35
+        self._partition()
         if shard is not None:
             shard.attach(self)
+
+    # -- the share ---------------------------------------------------------
+    @property
+    def attr_split(self) -> float:
+        return self._attr_split
+
+    @attr_split.setter
+    def attr_split(self, frac: float):
+        self._attr_split = float(frac)
+        self._partition()
+
+    def _split_on(self) -> bool:
+        return self._attr_split > 0.0
+
+    def _partition(self):
+        """Balanced shares of the current storage order (device-side; the
+        captured graphs read them at replay)."""
+        call("bh_partition", ptr(self.rp), self.n, self.world, W_POINT,
+             self._attr_split, self.cap, ptr(self.cuts), ptr(self.parts),
+             stream())
+
+    def share(self) -> tuple:
+        """(lo, hi) of this GPU's slots (synchronises)."""
+        p = self.part.cpu().numpy()
+        return int(p[0]), int(p[1])
 
     @property
     def rp(self):
@@ -353,25 +392,34 @@ class Engine:
         return self.csr[self.csr_key][2]
 
     # library kernels of one relabel (invert, 4 row gathers, CSR permute:
-    # 3 scan kernels + last offset + fill) and of one run's load / bounds /
-    # centre / store (3 gathers, 1, 1, 3 scatters)
-    KERNELS_PER_RELABEL = 10
+    # 3 scan kernels + last offset + fill, partition) and of one run's load /
+    # bounds / centre / store (3 gathers, 1, 1, 3 scatters)
+    KERNELS_PER_RELABEL = 11
     KERNELS_PER_RUN = 8
 
     def kernels_per_iteration(self, timed: bool = False) -> int:
         """Library kernel launches of one iteration: morton, sort histogram +
         one pass per code byte, 3 tree kernels, the summarize kernels (2 for
         the prefix summarize; else one per level below the top 7 plus one
-        for levels 6..0, tree.cu), the force
-        pass (1 fused or attractive +
-        repulsive), update; + the Z-partials sum when sharded."""
+        for levels 6..0, tree.cu), the side sweep, the force pass (1 fused
+        or 2), update; + Z sum, unpack and finish when sharded."""
         forces = 1 if self._fused(timed) else 2
         depth = self.code_bits // 2
         top = min(int(os.environ.get("BH_SUM_TOP", 6)), depth)  # tree.cu
         summarize = (2 if self.prefix_summary
                      else depth - top + (1 if top >= 0 else 0))
         return (1 + 1 + self.code_bits // 8 + 3 + summarize
-                + forces + 1 + (1 if self.shard is not None else 0))
+                + (1 if self._split_on() else 0) + forces + 1 + 1
+                + (6 if self.shard is not None else 0))
+
+    @property
+    def prefix_summary(self) -> bool:
+        # f32 runs summarize from the f64 prefix sums of the sorted points
+        # (2 launches; internal centres of mass differ from the reference's
+        # child-order sums by f64 rounding only); f64 runs keep the
+        # bit-exact level-by-level summarize.  The stage API's summarize()
+        # is always the bit-exact one.
+        return self.dtype == torch.float32
 
     # -- one iteration -----------------------------------------------------
     def _enqueue(self, ev=None):
@@ -379,95 +427,99 @@ class Engine:
         n, cb, t = self.n, self.code_bits, self.tree
         y = self.y
         rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
+        sharded = self.shard is not None
+        fused = self._fused(ev is not None)
         rec(0)
+        self._nvtx("tree")
         call(self.fn("bh_morton"), ptr(y), n, ptr(self.bounds), cb, 1,
              ptr(self.codes), st)
-        side = (self.shard is not None and self.shard_overlap
-                and ev is None)
-        # fused fast path: the first `split` CSR rows are swept on the side
-        # stream under the latency-bound tree build (they need only Y and P),
-        # the rest inside the fused force launch
-        split = self.split_rows() if self._fused(ev is not None) else 0
-        if split > 0:
+        if self._split_on():
+            # rows [lo, split) of the share are swept on the side stream
+            # under the latency-bound tree build (they need only Y and P)
             self.fork_ev.record(torch.cuda.current_stream())
             with torch.cuda.stream(self.side):
                 self.side.wait_event(self.fork_ev)
                 rec(7)
-                call(self.fn("bh_attractive"), ptr(self.rp), ptr(self.col),
-                     ptr(self.val), n, 1, ptr(y), 0, split, 1.0,
+                call(self.fn("bh_step_attractive"), ptr(self.rp),
+                     ptr(self.col), ptr(self.val), 1, ptr(y), ptr(self.part),
+                     int(math.ceil(self.cap * self._attr_split)) + 1,
                      ptr(self.sched), ptr(self.attr), stream())
-                rec(3)
-                self.join_ev.record(self.side)
-        if side:
-            # sharded fast path: this rank's attractive rows and their
-            # all-gather run on the side stream under the replicated tree
-            # build (dist.py)
-            self.fork_ev.record(torch.cuda.current_stream())
-            with torch.cuda.stream(self.side):
-                self.side.wait_event(self.fork_ev)
-                self.shard.attractive_side(self)
-                self.join_ev.record(self.side)
-        if self.shard is None and self.overlap:
-            # fork: the memory-bound CSR sweep needs only the centred Y, so
-            # it runs on a side stream under the latency-bound sort / tree /
-            # summarize chain and the issue-bound traversal
-            main = torch.cuda.current_stream()
-            self.fork_ev.record(main)
-            with torch.cuda.stream(self.side):
-                self.side.wait_event(self.fork_ev)
-                rec(7)
-                call(self.fn("bh_attractive"), ptr(self.rp), ptr(self.col),
-                     ptr(self.val), n, 1, ptr(y), 0, n, 1.0, ptr(self.sched),
-                     ptr(self.attr), stream())
                 rec(3)
                 self.join_ev.record(self.side)
         call("bh_sort", ptr(self.codes), n, cb, ptr(t.sorted_codes),
              ptr(t.order), ptr(self.ws_sort), self.ws_sort.numel(), st)
         t.build(y, st)
         rec(1)
+        self._nvtx("summarize")
         if self.prefix_summary:
             t.summarize_prefix(st)
         else:
             t.summarize(st)
         rec(2)
-        if self._fused(ev is not None):
+        self._nvtx("forces")
+        if sharded:
+            # this GPU's slots in the current Morton order
+            call("bh_step_qlist", ptr(t.order), n, ptr(self.part),
+                 ptr(self.qlist), ptr(self.ws_q), self.ws_q.numel(), st)
+
+        def forces(mode):
+            call(self.fn("bh_step_forces"), t.sref(), ptr(self.bounds),
+                 self.theta, ptr(y), ptr(self.rank_of), ptr(self.qlist),
+                 ptr(self.part), self.cap, mode, ptr(self.rep),
+                 ptr(self.zpart), ptr(self.ws_rep), self.ws_rep.numel(),
+                 ptr(self.rp), ptr(self.col), ptr(self.val), 1,
+                 ptr(self.sched), ptr(self.attr), st)
+
+        if fused:
             # both force passes in one launch, their CTAs sharing the SMs
             # (bitwise the same results as the two kernels)
-            call(self.fn("bh_forces"), t.sref(), ptr(self.bounds), self.theta, 0, n, 0,
-                 ptr(self.rep), None, ptr(self.z_dev), ptr(self.ws_rep),
-                 self.ws_rep.numel(), ptr(self.rp), ptr(self.col),
-                 ptr(self.val), n, 1, ptr(y), split, n, 1.0, ptr(self.sched),
-                 ptr(self.attr), st)
-            if split > 0:
-                torch.cuda.current_stream().wait_event(self.join_ev)
-            rec(4)
-            rec(5)
-            rep, rep_rank = self.rep, None
-        elif self.shard is None:
-            if not self.overlap:  # isolated kernels (stage breakdown)
-                rec(7)
-                call(self.fn("bh_attractive"), ptr(self.rp), ptr(self.col),
-                     ptr(self.val), n, 1, ptr(y), 0, n, 1.0, ptr(self.sched),
-                     ptr(self.attr), st)
-                rec(3)
-            call(self.fn("bh_repulsive"), t.sref(), ptr(self.bounds),
-                 self.theta, None, 0, n, 0, ptr(self.rep), None, None,
-                 ptr(self.z_dev), None, ptr(self.ws_rep), self.ws_rep.numel(),
-                 st)
-            rec(4)
-            if self.overlap:
-                torch.cuda.current_stream().wait_event(self.join_ev)
-            rec(5)
-            rep, rep_rank = self.rep, None
-        elif side:
-            rep, rep_rank = self.shard.repulsive(self, rec, st)
-            torch.cuda.current_stream().wait_event(self.join_ev)
+            forces(0)
         else:
-            rep, rep_rank = self.shard.forces(self, rec, st)
-        call(self.fn("bh_update"), ptr(y), ptr(self.v), ptr(self.g),
-             ptr(self.attr), ptr(rep), ptr(rep_rank), n, ptr(self.sched),
-             ptr(self.bounds), cb, ptr(self.ws_upd), self.ws_upd.numel(), st)
+            if not self._split_on():
+                rec(7)
+            forces(2)  # the sweep of rows [split, hi)
+            if not self._split_on():
+                rec(3)
+            rec(9)
+            forces(1)  # the traversal
+        if self._split_on():
+            torch.cuda.current_stream().wait_event(self.join_ev)
+        # Z: per-128-slot block sums of zpart (the other GPUs' blocks stay
+        # 0 for the all-reduce); one GPU folds them into sched.z at once
+        self._nvtx("z")
+        if sharded:
+            self.zblock.zero_()
+        call("bh_step_zsum", ptr(self.zpart), ptr(self.part), n, self.cap,
+             ptr(self.zblock), None if sharded else ptr(self.z_dev),
+             ptr(self.ws_zsum), self.ws_zsum.numel(), st)
+        rec(4)
+        if sharded:
+            self.shard.reduce_z(self)
+        rec(5)
+        self._nvtx("update")
+        call(self.fn("bh_step_update"), ptr(y), ptr(self.v), ptr(self.g),
+             ptr(self.attr), ptr(self.rep), ptr(self.part), n,
+             ptr(self.sched), ptr(self.bounds), cb, 0 if sharded else 1,
+             ptr(self.shard.ysend) if sharded else None, ptr(self.ws_upd),
+             self.ws_upd.numel(), st)
+        rec(8)
+        if sharded:
+            self._nvtx("comm")
+            self.shard.exchange_y(self)
         rec(6)
+        self._nvtx(None)
+
+    _nvtx_open = False
+
+    def _nvtx(self, name):
+        """NVTX range per stage (the StepTimings keys) around the enqueue of
+        an iteration: visible to nsys / ncu --nvtx on eager iterations; a
+        replayed graph shows as one "iteration" range (Engine._run)."""
+        if self._nvtx_open:
+            torch.cuda.nvtx.range_pop()
+        self._nvtx_open = name is not None
+        if name is not None:
+            torch.cuda.nvtx.range_push(name)
 
     def _capture(self, enqueue):
         """Capture `enqueue()` on the main stream into a CUDA graph.  The
@@ -488,9 +540,12 @@ class Engine:
         return [[torch.cuda.Event(enable_timing=True, external=True)
                  for _ in range(self.N_EVENTS)] for _ in range(k)]
 
+    def _key(self, *head):
+        return head + (self.csr_key, self._fused(head[0] == "timed"),
+                       self._split_on())
+
     def _graph(self, k):
-        key = (k, self.csr_key, self.overlap, self._fused(True),
-               self.attr_split)
+        key = self._key("timed", k)
         if key not in self.graphs:
             evs = self._events(k)
             g = self._capture(lambda: [self._enqueue(evs[i]) for i in range(k)])
@@ -500,8 +555,7 @@ class Engine:
     def _graph1(self):
         """One iteration without timing events (the fast path: replayed
         back to back, the host only syncs at chunk boundaries)."""
-        key = ("fast", self.csr_key, self.overlap, self._fused(False),
-               self.shard_overlap, self.attr_split)
+        key = self._key("fast")
         if key not in self.graphs:
             self.graphs[key] = self._capture(lambda: self._enqueue(None))
         return self.graphs[key]
@@ -510,8 +564,7 @@ class Engine:
         """graph_chunk iterations in one graph without timing events: one
         graph launch per chunk instead of one per iteration."""
         k = self.cfg.graph_chunk
-        key = ("fastk", k, self.csr_key, self.overlap, self._fused(False),
-               self.shard_overlap, self.attr_split)
+        key = self._key("fastk", k)
         if key not in self.graphs:
             self.graphs[key] = self._capture(
                 lambda: [self._enqueue(None) for _ in range(k)])
@@ -557,15 +610,20 @@ class Engine:
 
     def store(self):
         """Storage order -> point-id order (Embedding)."""
+        if self.shard is not None:
+            self.shard.gather_state(self)
         e = self.e
         for src, dst in ((self.y, e.y), (self.v, e.v), (self.g, e.g)):
             self._rows("bh_scatter_rows", src, self.ids, dst)
 
     def relabel(self):
-        """Renumber the storage slots in the last tree's Morton order."""
+        """Renumber the storage slots in the last tree's Morton order and
+        re-balance the shares."""
+        if self.shard is not None:
+            self.shard.gather_state(self)  # v, g of every slot
         st = stream()
         order = self.tree.order
-        call("bh_invert_perm", ptr(order), self.n, ptr(self.rank), st)
+        call("bh_invert_perm", ptr(order), self.n, ptr(self.perm_inv), st)
         for buf in (self.y, self.v, self.g):
             self._rows("bh_gather_rows", buf, order, self.tmp)
             buf.copy_(self.tmp)
@@ -576,10 +634,23 @@ class Engine:
         rp, col, val = self.csr[self.csr_key]
         orp, ocol, oval = self.csr[nxt]
         call(self.fn("bh_permute_csr"), ptr(rp), ptr(col), ptr(val),
-             ptr(order), ptr(self.rank), self.n, ptr(orp), ptr(ocol),
+             ptr(order), ptr(self.perm_inv), self.n, ptr(orp), ptr(ocol),
              ptr(oval), ptr(self.ws_perm), self.ws_perm.numel(), st)
         self.csr_key = nxt
+        self._partition()
         self.since_relabel = 0
+        self.relabeled = True
+
+    def _initial_relabel(self):
+        """Morton order of the starting Y (shift 0) as the storage order."""
+        st = stream()
+        n, cb, t = self.n, self.code_bits, self.tree
+        call(self.fn("bh_morton"), ptr(self.y), n, ptr(self.bounds), cb, 0,
+             ptr(self.codes), st)
+        call("bh_sort", ptr(self.codes), n, cb, ptr(t.sorted_codes),
+             ptr(t.order), ptr(self.ws_sort), self.ws_sort.numel(), st)
+        self.relabel()
+        self.launches += 2 + self.code_bits // 8 + self.KERNELS_PER_RELABEL
 
     # -- driver --------------------------------------------------------------
     def begin(self):
@@ -605,8 +676,10 @@ class Engine:
 
     def _check(self):
         s = _lib.read_struct(self.sched, SCHED_DTYPE)
-        if int(s["bad"]) != INT64_MAX:
-            bad = int(s["bad"])
+        bad = int(s["bad"])
+        if self.shard is not None:
+            bad = self.shard.min_host(self, bad)
+        if bad != INT64_MAX:
             slot = bad & 0xFFFFFFFF
             point = int(self.ids[slot].item())
             raise ValueError(f"non-finite gradient at point {point} "
@@ -631,6 +704,8 @@ class Engine:
         self.launches += self.KERNELS_PER_RUN
         self.load()
         self.begin()
+        if self.relabel_every and not self.relabeled:
+            self._initial_relabel()
         done = 0
         chunk = self.cfg.graph_chunk
         while done < n_iter:
@@ -642,7 +717,9 @@ class Engine:
                 else:
                     g = self._graph1()
                     for _ in range(k):
+                        torch.cuda.nvtx.range_push("iteration")
                         g.replay()
+                        torch.cuda.nvtx.range_pop()
             elif use_graph:
                 g, evs = self._graph(k)
                 g.replay()
@@ -653,15 +730,8 @@ class Engine:
             done += k
             self.launches += k * self.kernels_per_iteration(timings is not None)
             self.since_relabel += k
-            relabel = (self.relabel_every and done < n_iter
-                       and self.since_relabel >= self.relabel_every)
-            if relabel:
-                r0 = torch.cuda.Event(enable_timing=True)
-                r1 = torch.cuda.Event(enable_timing=True)
-                r0.record()
-                self.relabel()
-                r1.record()
-                self.launches += self.KERNELS_PER_RELABEL
+            # the chunk's non-finite check comes first: a bad gradient names
+            # its point through the ids of the storage order it was found in
             self.main.synchronize()
             self._check()
             if timings is not None:
@@ -669,8 +739,20 @@ class Engine:
                     for name, (a, b) in self._stage_events().items():
                         timings.add(name, evs[i][a].elapsed_time(evs[i][b]) * 1e-3)
                     if self.shard is not None:
-                        timings.add("comm", evs[i][4].elapsed_time(evs[i][5]) * 1e-3)
-                if relabel:
+                        timings.add("comm", (evs[i][4].elapsed_time(evs[i][5])
+                                             + evs[i][8].elapsed_time(evs[i][6])) * 1e-3)
+            relabel = (self.relabel_every and done < n_iter
+                       and self.since_relabel >= self.relabel_every)
+            if relabel:
+                r0 = torch.cuda.Event(enable_timing=True)
+                r1 = torch.cuda.Event(enable_timing=True)
+                r0.record()
+                torch.cuda.nvtx.range_push("relabel")
+                self.relabel()
+                torch.cuda.nvtx.range_pop()
+                r1.record()
+                self.launches += self.KERNELS_PER_RELABEL
+                if timings is not None:
                     r1.synchronize()
                     timings.add("relabel", r0.elapsed_time(r1) * 1e-3)
         self.end()
@@ -681,7 +763,6 @@ class Engine:
     def z(self) -> float:
         return float(_lib.read_struct(self.sched, SCHED_DTYPE)["z"])
 
-
 def gradient_step(e: Embedding, p: SparseAffinity, cfg: TsneConfig,
                   buffers: GradientBuffers | None = None,
                   timings: StepTimings | None = None) -> Embedding:
@@ -689,15 +770,19 @@ def gradient_step(e: Embedding, p: SparseAffinity, cfg: TsneConfig,
     (optimizer.py:195-224); the exaggeration is the one ``p`` carries."""
     cfg.validate()
     eng = getattr(e, "_engine", None)
+    # the engine copies theta and the schedule constants: key its cache on
+    # the config's values, so an in-place change of cfg takes effect (the
+    # reference reads cfg on every step)
+    snap = astuple(cfg)
     if (eng is None or eng.p.base_values is not p.base_values
-            or getattr(e, "_engine_cfg", None) is not cfg):
+            or getattr(e, "_engine_cfg", None) != snap):
         # the embedding's dtype is the run precision, as in the reference
         # (optimizer.py:200, 214)
         prec = "f64" if e.y.dtype == torch.float64 else "f32"
         run_cfg = cfg if cfg.precision == prec else replace(cfg, precision=prec)
         eng = Engine(p, e, run_cfg, schedule=False)
         e._engine = eng
-        e._engine_cfg = cfg
+        e._engine_cfg = snap
     eng.set_iteration(e.iteration, exaggeration=p.exaggeration)
     eng.run(1, timings, use_graph=False)
     if buffers is not None:
@@ -765,11 +850,16 @@ def affinities(x, cfg: TsneConfig, knn=None, timings=None):
     return p, graph
 
 
-def run(x, cfg: TsneConfig, *, knn=None) -> tuple:
+def run(x, cfg: TsneConfig, *, knn=None, profile: bool = False) -> tuple:
     """Full pipeline; returns (embedding, timings, final exact KL)
     (optimizer.py:289-332).  ``knn``: a NeighborGraph / (indices,
     sq_distances) computed once by the reference (north star), else the
-    exact kNN is computed on the GPU."""
+    exact kNN is computed on the GPU.  ``profile``: time the stages with
+    separate, non-overlapping kernels (attractive and repulsive apart, no
+    side-stream sweep) so that the per-stage times add up; otherwise the
+    fast pipeline runs and the timings carry "forces" (the fused launch,
+    end of summarize to the join) and "attractive" (the side-stream sweep,
+    concurrent with the tree build)."""
     cfg.validate()
     tick = time.perf_counter
     wall0 = tick()
@@ -779,11 +869,11 @@ def run(x, cfg: TsneConfig, *, knn=None) -> tuple:
     p, _ = affinities(x, cfg, knn=knn, timings=timings)
     e = init_embedding(n, cfg.seed, dtype=cfg.dtype)
     eng = Engine(p, e, cfg, schedule=True)
-    # the fast pipeline (side sweep + fused force launch), evented: the
-    # timings carry "forces" (the fused launch, end of summarize to the join)
-    # and "attractive" (the side-stream sweep, concurrent with the tree build)
-    # instead of separate attractive / repulsive kernels
-    eng.fuse_timed = True
+    if profile:
+        eng.fuse_timed = False
+        eng.attr_split = 0.0
+    else:
+        eng.fuse_timed = True
     kl_history = []
     done = 0
     while done < cfg.n_iter:

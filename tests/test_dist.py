@@ -1,10 +1,14 @@
 """Multi-rank host logic of the sharded loop (paper_2212_11506_b200/dist.py)
 on CPU with gloo, world sizes 2 and 3.
 
-Each rank computes its shard of the forces with the CPU oracle (the stand-in
-for the CUDA kernels here), the shards are exchanged with all_gather_into_
-tensor exactly as Shard lays them out, and the assembled gradient and Z
-must equal the single-process result bit for bit -- the property that makes
+Each rank takes its cost-balanced share of the storage slots
+(``balanced_cuts``, the host mirror of bh_partition), computes the forces of
+its share with the CPU oracle (the stand-in for the CUDA kernels here),
+writes its Z partials (one per 128 slots, zero outside the share), the
+partials are all-reduced, the rank updates its own slots, packs them into a
+cap-row send buffer and the shares are all-gathered and unpacked by the
+cuts -- exactly the buffers and collectives of Shard.  The assembled Y and Z
+must equal the single-process result bit for bit: the property that makes
 the GPU trajectory independent of the GPU count.
 """
 
@@ -18,7 +22,8 @@ torch = pytest.importorskip("torch")
 import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
-from paper_2212_11506_b200.dist import POINTS_PER_PARTIAL, ShardPlan  # noqa: E402
+from paper_2212_11506_b200.dist import (POINTS_PER_PARTIAL, W_POINT,  # noqa: E402
+                                        balanced_cuts, equal_share, share_cap)
 
 
 def fixed_sum(x):
@@ -45,25 +50,25 @@ def problem():
     return y, ro, co, va
 
 
-def shard_forces(o, y, ro, co, va, plan):
-    """What one rank's kernels produce: attr rows, sorted-order rep, Z
-    partials of its POINTS_PER_PARTIAL-point blocks."""
+def step_parts(o, y, ro, co, va):
+    """Per-point forces and per-128-slot Z partials of one iteration, and
+    the elementwise update of every point (storage order = ids here)."""
     n = y.shape[0]
     t = o.build_tree(y, code_bits=32)          # replicated tree
     a0, a1 = o.attractive(ro, co, va, y)
     r0, r1, zp, _ = o.repulsive_bh(t, y, 0.5)
-    lo, hi = plan.mine
-    attr = np.zeros((plan.chunk, 2), np.float32)
-    attr[:hi - lo] = np.column_stack([a0, a1])[lo:hi]
-    rep = np.zeros((plan.chunk, 2), np.float32)
-    rep[:hi - lo] = np.column_stack([r0, r1])[t.order[lo:hi]]
-    z = np.zeros(plan.partials_per_rank)
-    zs = zp[t.order]
-    for b in range(plan.partials_per_rank):
-        s, e = lo + b * POINTS_PER_PARTIAL, min(hi, lo + (b + 1) * POINTS_PER_PARTIAL)
-        if s < e:
-            z[b] = np.sum(zs[s:e])
-    return attr, rep, z, t.order
+    nb = (n + POINTS_PER_PARTIAL - 1) // POINTS_PER_PARTIAL
+    zblk = np.array([np.sum(zp[b * POINTS_PER_PARTIAL:(b + 1) * POINTS_PER_PARTIAL])
+                     for b in range(nb)])
+    return (a0, a1), (r0, r1), zblk
+
+
+def updated(o, y, attr, rep, z):
+    s = o.State(np.ascontiguousarray(y[:, 0]), np.ascontiguousarray(y[:, 1]),
+                np.zeros(y.shape[0], np.float32), np.zeros(y.shape[0], np.float32),
+                np.ones(y.shape[0], np.float32), np.ones(y.shape[0], np.float32))
+    o.update(s, attr, rep, z, 0.5)
+    return np.column_stack([s.y0, s.y1])
 
 
 def worker(rank, world, port, q):
@@ -74,21 +79,30 @@ def worker(rank, world, port, q):
         o.build()
         y, ro, co, va = problem()
         n = y.shape[0]
-        plan = ShardPlan(n, world, rank)
-        attr, rep, z, order = shard_forces(o, y, ro, co, va, plan)
-        A = torch.zeros((plan.gathered_len(), 2))
-        R = torch.zeros((plan.gathered_len(), 2))
-        Z = torch.zeros(world * plan.partials_per_rank, dtype=torch.float64)
-        dist.all_gather_into_tensor(A, torch.from_numpy(attr))
-        dist.all_gather_into_tensor(R, torch.from_numpy(rep))
-        dist.all_gather_into_tensor(Z, torch.from_numpy(z))
-        rank_of = np.empty(n, np.int64)
-        rank_of[order] = np.arange(n)
-        attr_full = A.numpy()[:n]
-        rep_full = R.numpy()[rank_of]
-        zt = fixed_sum(Z.numpy())
+        cap = share_cap(n, world)
+        cuts = balanced_cuts(ro, n, world, cap=cap)
+        lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+        attr, rep, zblk = step_parts(o, y, ro, co, va)
+        # this rank's Z partials; the others' stay zero
+        z = np.zeros_like(zblk)
+        z[lo // POINTS_PER_PARTIAL:(hi + POINTS_PER_PARTIAL - 1) // POINTS_PER_PARTIAL] = \
+            zblk[lo // POINTS_PER_PARTIAL:(hi + POINTS_PER_PARTIAL - 1) // POINTS_PER_PARTIAL]
+        zt = torch.from_numpy(z)
+        dist.all_reduce(zt)
+        ztot = fixed_sum(zt.numpy())
+        # the share's update, packed into the cap-row send buffer
+        ynew = updated(o, y, attr, rep, ztot)
+        send = np.zeros((cap, 2), np.float32)
+        send[:hi - lo] = ynew[lo:hi]
+        gbuf = torch.zeros((world * cap, 2))
+        dist.all_gather_into_tensor(gbuf, torch.from_numpy(send))
+        g = gbuf.numpy()
+        y_all = np.empty_like(y)
+        for r in range(world):  # bh_unpack_rows
+            a, b = int(cuts[r]), int(cuts[r + 1])
+            y_all[a:b] = g[r * cap:r * cap + (b - a)]
         if rank == 0:
-            q.put((attr_full, rep_full, zt))
+            q.put((y_all, ztot))
     finally:
         dist.destroy_process_group()
 
@@ -99,33 +113,48 @@ def free_port():
         return s.getsockname()[1]
 
 
-def test_shard_plan_ranges_cover_and_align():
+def test_balanced_cuts_cover_align_and_cap():
+    rng = np.random.default_rng(1)
     for n in (1, 255, 256, 1000, 70_000, 1_300_000):
+        lens = rng.integers(90, 400, n)
+        lens[rng.integers(0, n, max(1, n // 50))] = 1200  # heavy rows
+        rp = np.concatenate([[0], np.cumsum(lens)])
         for world in (1, 2, 3, 4, 8):
-            ranges = [ShardPlan(n, world, r).mine for r in range(world)]
-            assert ranges[0][0] == 0 and ranges[-1][1] == n
-            for (a, b), (c, d) in zip(ranges, ranges[1:]):
-                assert b == c
-            chunk = ShardPlan(n, world, 0).chunk
-            assert chunk % POINTS_PER_PARTIAL == 0
-            for a, _ in ranges:
-                assert a % POINTS_PER_PARTIAL == 0 or a == n
+            cuts = balanced_cuts(rp, n, world)
+            cap = share_cap(n, world)
+            assert cuts[0] == 0 and cuts[-1] == n
+            assert np.all(np.diff(cuts) >= 0)
+            assert np.all(np.diff(cuts) <= cap)
+            assert np.all((cuts[:-1] % POINTS_PER_PARTIAL == 0) | (cuts[:-1] == n))
+
+
+def test_balanced_cuts_balance_cost():
+    """Ranges follow the cost (W_POINT per point + row length), not the
+    point count: a skewed row-length profile gets unequal point counts and
+    near-equal costs."""
+    n, world = 200_000, 8
+    lens = np.where(np.arange(n) < n // 4, 1000, 90)  # heavy first quarter
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    cuts = balanced_cuts(rp, n, world)
+    cost = np.array([W_POINT * (cuts[r + 1] - cuts[r]) + rp[cuts[r + 1]] - rp[cuts[r]]
+                     for r in range(world)])
+    assert cost.max() / cost.mean() < 1.01
+    assert len(set(np.diff(cuts).tolist())) > 1
+    # a balanced range above the cap falls back to equal shares
+    eq = balanced_cuts(rp, n, world, cap=equal_share(n, world))
+    assert np.all(np.diff(eq)[:-1] == equal_share(n, world))
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_forces_equal_single_process(oracle, world):
+def test_sharded_step_equals_single_process(oracle, world):
     y, ro, co, va = problem()
-    n = y.shape[0]
-    attr1, rep1, z1, order1 = shard_forces(oracle, y, ro, co, va,
-                                           ShardPlan(n, 1, 0))
-    rank_of = np.empty(n, np.int64)
-    rank_of[order1] = np.arange(n)
-    ref_attr, ref_rep, ref_z = attr1[:n], rep1[rank_of], fixed_sum(z1)
+    attr, rep, zblk = step_parts(oracle, y, ro, co, va)
+    ref_z = fixed_sum(zblk)
+    ref_y = updated(oracle, y, attr, rep, ref_z)
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     mp.start_processes(worker, args=(world, free_port(), q), nprocs=world,
                        join=True, start_method="spawn")
-    attr, rep, z = q.get()
-    np.testing.assert_array_equal(attr, ref_attr)
-    np.testing.assert_array_equal(rep, ref_rep)
+    y_all, z = q.get()
     assert z == ref_z  # bitwise: Z independent of the world size
+    np.testing.assert_array_equal(y_all, ref_y)

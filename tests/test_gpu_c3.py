@@ -1,0 +1,127 @@
+"""Parity at the headline configuration C3 (BASELINE.json configs[3]:
+N = 1.3M, D = 50, K = 90, perplexity 30, theta 0.5, the 1000-iteration
+schedule) against the UNMODIFIED reference's own run and the C oracle.
+
+tests/golden/c3_run.npz was made in the dev container by
+tests/golden/make_c3.py: the reference's run() (optimizer.py:289-332, numba,
+f32) on the seeded C3 data with its exact kNN graph (knn.py:36-59
+semantics), recording the final exact KL, the BH KL every 250 iterations,
+Y at the start of iterations 250, 500 and 999, and a SHA-256 of the graph.
+
+* the GPU exact kNN (bh_knn) reproduces that graph bit for bit;
+* the GPU BSP betas are within 1e-5 of the oracle's on all 1.3M rows;
+* the gradient at the reference trajectory's own Y (iterations 0, 250, 500,
+  999, exaggeration 12 before 250) is within 1e-4 rel-L2 of the oracle's;
+* the final KL of the whole GPU pipeline is within 1% of the reference's
+  (the trajectory itself is chaotic), the periodic KL within 5%.
+"""
+
+import hashlib
+import time
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bh():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2212_11506_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return golden("c3_run")
+
+
+@pytest.fixture(scope="module")
+def c3(bh):
+    from paper_2212_11506_b200.workloads import c3 as gen
+    x = gen()
+    t0 = time.time()
+    g = bh.knn_exact(x, 90)
+    torch.cuda.synchronize()
+    print(f"\n[c3] GPU exact kNN {time.time() - t0:.1f}s")
+    return x, g
+
+
+def graph_sha(idx, sqd):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(idx, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(sqd, dtype=np.float32).tobytes())
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module")
+def c3p(bh, c3):
+    x, g = c3
+    pr = bh.calibrate_perplexity(g, 30.0)
+    p = bh.symmetrize(pr, g)
+    return pr, p
+
+
+def test_c3_knn_graph_equals_reference_semantics(c3, ref):
+    _, g = c3
+    sha = graph_sha(g.indices.cpu().numpy(), g.sq_distances.cpu().numpy())
+    assert sha == str(ref["knn_sha256"])
+
+
+def test_c3_bsp_betas_vs_oracle(bh, oracle, c3, c3p):
+    _, g = c3
+    pr, _ = c3p
+    sqd = g.sq_distances.cpu().numpy()
+    t0 = time.time()
+    betas, cond = oracle.calibrate_perplexity(sqd, 30.0)
+    print(f"\n[c3] oracle BSP {time.time() - t0:.1f}s")
+    got = pr.betas.cpu().numpy()
+    rel = np.abs(got - betas) / np.abs(betas)
+    assert rel.max() <= 1e-5, (rel.max(), int(rel.argmax()))
+    gc = pr.conditional.cpu().numpy()
+    assert np.abs(gc - cond).max() <= 1e-5 * np.abs(cond).max()
+
+
+@pytest.mark.parametrize("it", [0, 250, 500, 999])
+def test_c3_gradient_on_reference_trajectory(bh, oracle, c3p, ref, it):
+    _, p = c3p
+    if it == 0:
+        rng = np.random.Generator(np.random.Philox(0))
+        y = (rng.standard_normal((p.n, 2)) * 1e-4).astype(np.float32)
+    else:
+        y = ref[f"y{it}"]
+    exag = 12.0 if it < 250 else 1.0
+    pe = bh.set_exaggeration(p, exag)
+    ro, co, va = pe.to_reference()
+    g0, g1, _, _, z = oracle.gradient(y, ro, co, va, 0.5, code_bits=32)
+    want = np.column_stack([g0, g1]).astype(np.float64)
+    c, r = bh.compute_bounds(y)
+    t = bh.summarize(bh.build_tree(bh.morton_codes(y, c, r), y))
+    buf = bh.GradientBuffers.allocate(p.n)
+    bh.attractive(pe, y, buf)
+    bh.repulsive_bh(t, y, 0.5, buf)
+    assert buf.z == pytest.approx(z, rel=1e-6)
+    zf = np.float32(buf.z)
+    got = 4.0 * (buf.attr.cpu().numpy().astype(np.float64)
+                 - buf.rep.cpu().numpy().astype(np.float64) / zf)
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"\n[c3] iteration {it}: gradient rel-L2 {rel:.2e}")
+    assert rel <= 1e-4, rel
+
+
+def test_c3_full_run_final_kl_within_1pct(bh, c3, ref):
+    x, g = c3
+    e, timings, kl = bh.run(x, bh.TsneConfig(kl_every=250), knn=g)
+    want = float(ref["kl"])
+    print(f"\n[c3] final KL {kl:.5f} (reference {want:.5f}), "
+          f"run() wall {timings.total_wall_s:.1f}s")
+    assert abs(kl - want) / want < 0.01, (kl, want)
+    ours = [k for _, k in timings.kl_history]
+    theirs = [float(k) for _, k in ref["kl_history"]]
+    assert len(ours) == len(theirs) == 4
+    assert all(abs(a - b) / b < 0.05 for a, b in zip(ours, theirs)), (ours, theirs)
