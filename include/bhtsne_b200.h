@@ -151,6 +151,17 @@ int bh_bounds(const float *y, int64_t n, int code_bits, bh_bounds_t *out,
  * (shift0, shift1) (the fused update/centering of gradient_step). */
 int bh_morton(float *y, int64_t n, const bh_bounds_t *bounds, int code_bits,
               int apply_shift, void *codes, bh_stream_t stream);
+/* The engine's tree order: the same quantisation, keyed by the Hilbert
+ * index of the cell instead of the Morton interleave.  The top 2d bits still
+ * name the depth-d cell, so the canonical tree over these keys has exactly
+ * the reference tree's cells and leaves, siblings ordered along the curve;
+ * consecutive points are then always neighbours (no Morton jumps), which
+ * keeps the traversal's warps coherent.  Not a reference interface. */
+int bh_hilbert(float *y, int64_t n, const bh_bounds_t *bounds, int code_bits,
+               int apply_shift, void *codes, bh_stream_t stream);
+int bh_hilbert_f64(double *y, int64_t n, const bh_bounds_t *bounds,
+                   int code_bits, int apply_shift, void *codes,
+                   bh_stream_t stream);
 int bh_bounds_f64(const double *y, int64_t n, int code_bits, bh_bounds_t *out,
                   void *ws, size_t ws_bytes, bh_stream_t stream);
 int bh_morton_f64(double *y, int64_t n, const bh_bounds_t *bounds,

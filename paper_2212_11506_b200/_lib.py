@@ -69,6 +69,8 @@ SIGNATURES = {
     "bh_bounds_workspace_bytes": ([_I64], _SZ),
     "bh_bounds": ([_P, _I64, C.c_int, _P, _P, _SZ, _P], C.c_int),
     "bh_morton": ([_P, _I64, _P, C.c_int, C.c_int, _P, _P], C.c_int),
+    "bh_hilbert": ([_P, _I64, _P, C.c_int, C.c_int, _P, _P], C.c_int),
+    "bh_hilbert_f64": ([_P, _I64, _P, C.c_int, C.c_int, _P, _P], C.c_int),
     "bh_sort_workspace_bytes": ([_I64, C.c_int], _SZ),
     "bh_sort": ([_P, _I64, C.c_int, _P, _P, _P, _SZ, _P], C.c_int),
     "bh_sort_pairs": ([_P, _P, _I64, C.c_int, _P, _P, _P, _SZ, _P], C.c_int),

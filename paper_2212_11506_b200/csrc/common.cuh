@@ -145,6 +145,24 @@ template <> struct NodeRec<double> {
 
 }  // namespace bh
 
+// Device-side checks of a debug build (-DBH_DEBUG, tools/build_variant.py):
+// compute-sanitizer is unavailable on this GPU pool, so the kernels' own
+// invariants (traversal stack bounds, node indices, share ranges) trap.
+#ifdef BH_DEBUG
+#include <cstdio>
+#define BH_DASSERT(c)                                                         \
+    do {                                                                      \
+        if (!(c)) {                                                           \
+            printf("BH_DASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);  \
+            __trap();                                                         \
+        }                                                                     \
+    } while (0)
+#else
+#define BH_DASSERT(c) \
+    do {              \
+    } while (0)
+#endif
+
 #define BH_CHECK_LAUNCH(what)                                           \
     do {                                                                      \
         cudaError_t e_ = cudaGetLastError();                                  \

@@ -84,6 +84,7 @@ __global__ void k_unpack(const E *__restrict__ gbuf, int64_t cap,
          i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / cap);
         const int64_t j = i - (int64_t)r * cap, lo = cuts[r];
+        BH_DASSERT(cuts[r + 1] - lo <= cap);
         if (j < cuts[r + 1] - lo) dst[lo + j] = gbuf[i];
     }
 }

@@ -133,6 +133,7 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
                                          Acc64 &a64, RepCounts &cn,
                                          uint4 *stk, int &sp) {
     float4 rec[CNT];  // all loads issued up front (ILP)
+    BH_DASSERT(first + CNT <= (uint32_t)BH_CHILD_MASK);
 #pragma unroll
     for (int c = 0; c < CNT; c++) rec[c] = __ldg(&g.node[first + c]);
     float fz = 0.f, fx = 0.f, fy = 0.f;
@@ -284,6 +285,7 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
     if (valid) {
         if (slots && A.qlist) {
             slot = A.qlist[t];
+            BH_DASSERT(slot >= A.part->lo && slot < A.part->hi);
             yi = A.y_query[slot];
             if (!SC) self = (uint32_t)A.rank[slot];
         } else if (slots) {
@@ -315,6 +317,7 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         // `ent`, so all reads complete before any lane overwrites the slot;
         // the barrier at the end of the loop orders the pushes before the
         // next read)
+        BH_DASSERT(sp >= 1 && sp <= CAP);
         const uint4 ent = stk[--sp];
         const uint32_t first = ent.x & BH_CHILD_MASK;
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
@@ -346,6 +349,7 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
             else
                 bh_group_leaves<1, COUNT, SC>(g, first, a, cn);
         }
+        BH_DASSERT(sp <= CAP);  // the pushes stayed inside this warp's stack
         __syncwarp();
     }
     z = a.z;

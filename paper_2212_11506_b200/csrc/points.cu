@@ -223,7 +223,35 @@ __device__ __forceinline__ double2 shifted(double2 p, const bh_bounds_t *b) {
                         __dsub_rn(p.y, b->shift1_f64));
 }
 
-template <int BITS, typename T>
+// Hilbert index of the quantised cell (m0, m1), BITS/2 bits per dimension,
+// the classic rotate-and-reflect walk from the top bit.  The top 2d bits of
+// the index name the depth-d quadtree cell of the point (a bijection at
+// every level), so the canonical tree over Hilbert keys has exactly the
+// Morton tree's cells -- only siblings are ordered along the curve, which
+// has no jumps between consecutive points.
+template <int BITS, typename U>
+__device__ __forceinline__ U hilbert_key(U x, U y) {
+    constexpr int H = BITS / 2;
+    constexpr U full = (U)((1ull << H) - 1ull);
+    U d = 0;
+#pragma unroll
+    for (int l = H - 1; l >= 0; l--) {
+        const U rx = (x >> l) & 1u, ry = (y >> l) & 1u;
+        d = (d << 2) | ((3u * rx) ^ ry);
+        if (ry == 0) {
+            if (rx == 1) {
+                x = full - x;
+                y = full - y;
+            }
+            const U t = x;
+            x = y;
+            y = t;
+        }
+    }
+    return d;
+}
+
+template <int BITS, typename T, bool HILBERT = false>
 __global__ void __launch_bounds__(kPtThreads)
 k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
          int apply_shift,
@@ -244,10 +272,12 @@ k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
         double q1 = __dmul_rn(__dsub_rn((double)p.y, root1), scale);
         if constexpr (BITS == 32) {
             uint32_t m0 = __double2uint_rz(q0), m1 = __double2uint_rz(q1);
-            codes[i] = spread16(m0) | (spread16(m1) << 1);
+            codes[i] = HILBERT ? hilbert_key<32>(m0, m1)
+                               : spread16(m0) | (spread16(m1) << 1);
         } else {
             uint64_t m0 = __double2ull_rz(q0), m1 = __double2ull_rz(q1);
-            codes[i] = spread32(m0) | (spread32(m1) << 1);
+            codes[i] = HILBERT ? hilbert_key<64>(m0, m1)
+                               : spread32(m0) | (spread32(m1) << 1);
         }
     }
 }
@@ -455,18 +485,18 @@ static int bounds_impl(const T *y, int64_t n, int code_bits, bh_bounds_t *out,
     return BH_OK;
 }
 
-template <typename T>
+template <typename T, bool HILBERT = false>
 static int morton_impl(T *y, int64_t n, const bh_bounds_t *bounds,
                        int code_bits, int apply_shift, void *codes,
                        bh_stream_t stream) {
     BH_REQUIRE(n >= 1, "need at least one point");
     int grid = pt_grid(n);
     if (code_bits == 32)
-        BH_LAUNCH("k_morton", (k_morton<32, T>), grid, kPtThreads, 0,
+        BH_LAUNCH("k_morton", (k_morton<32, T, HILBERT>), grid, kPtThreads, 0,
                   bh_cs(stream), (p2_t<T> *)y, n, bounds, apply_shift,
                   (uint32_t *)codes);
     else if (code_bits == 64)
-        BH_LAUNCH("k_morton", (k_morton<64, T>), grid, kPtThreads, 0,
+        BH_LAUNCH("k_morton", (k_morton<64, T, HILBERT>), grid, kPtThreads, 0,
                   bh_cs(stream), (p2_t<T> *)y, n, bounds, apply_shift,
                   (uint64_t *)codes);
     else
@@ -557,6 +587,20 @@ extern "C" int bh_morton_f64(double *y, int64_t n, const bh_bounds_t *bounds,
                              int code_bits, int apply_shift, void *codes,
                              bh_stream_t stream) {
     return morton_impl(y, n, bounds, code_bits, apply_shift, codes, stream);
+}
+
+extern "C" int bh_hilbert(float *y, int64_t n, const bh_bounds_t *bounds,
+                          int code_bits, int apply_shift, void *codes,
+                          bh_stream_t stream) {
+    return morton_impl<float, true>(y, n, bounds, code_bits, apply_shift,
+                                    codes, stream);
+}
+
+extern "C" int bh_hilbert_f64(double *y, int64_t n, const bh_bounds_t *bounds,
+                              int code_bits, int apply_shift, void *codes,
+                              bh_stream_t stream) {
+    return morton_impl<double, true>(y, n, bounds, code_bits, apply_shift,
+                                     codes, stream);
 }
 
 extern "C" int bh_update(float *y, float *v, float *g, const float *attr,

@@ -69,6 +69,11 @@ class TsneConfig:
     code_bits: int = DEFAULT_CODE_BITS
     graph_chunk: int = 25
     relabel_every: int = 50  # Morton renumbering period (0: never)
+    # the engine's tree order: "hilbert" keys (the same cells and leaves as
+    # the reference's Morton tree, siblings along the Hilbert curve: no
+    # jumps between consecutive points, 6.5% faster traversal at C3) or
+    # "morton" (the reference's sibling order); the stage API is Morton
+    curve: str = "hilbert"
 
     def validate(self) -> "TsneConfig":
         if self.perplexity <= 1:
@@ -99,6 +104,9 @@ class TsneConfig:
             raise ValueError("graph_chunk must be >= 1")
         if self.relabel_every < 0:
             raise ValueError("relabel_every must be >= 0")
+        if self.curve not in ("hilbert", "morton"):
+            raise ValueError(f"curve must be 'hilbert' or 'morton', got "
+                             f"{self.curve!r}")
         return self
 
     @property
@@ -257,6 +265,7 @@ class Engine:
             raise ValueError(f"matrix is over {p.n} points, embedding has {n}")
         self.n, self.cfg, self.e, self.p = n, cfg, e, p
         self.code_bits = cfg.code_bits
+        self.keys = "bh_hilbert" if cfg.curve == "hilbert" else "bh_morton"
         dev = e.y.device
         self.dev = dev
         dt = _lib.torch_dtype(cfg.precision)
@@ -431,7 +440,7 @@ class Engine:
         fused = self._fused(ev is not None)
         rec(0)
         self._nvtx("tree")
-        call(self.fn("bh_morton"), ptr(y), n, ptr(self.bounds), cb, 1,
+        call(self.fn(self.keys), ptr(y), n, ptr(self.bounds), cb, 1,
              ptr(self.codes), st)
         if self._split_on():
             # rows [lo, split) of the share are swept on the side stream
@@ -645,7 +654,7 @@ class Engine:
         """Morton order of the starting Y (shift 0) as the storage order."""
         st = stream()
         n, cb, t = self.n, self.code_bits, self.tree
-        call(self.fn("bh_morton"), ptr(self.y), n, ptr(self.bounds), cb, 0,
+        call(self.fn(self.keys), ptr(self.y), n, ptr(self.bounds), cb, 0,
              ptr(self.codes), st)
         call("bh_sort", ptr(self.codes), n, cb, ptr(t.sorted_codes),
              ptr(t.order), ptr(self.ws_sort), self.ws_sort.numel(), st)
