@@ -430,8 +430,19 @@ def summarize_ncu(table):
     whole profiled fused iteration."""
     if not table:
         return None
-    res = {}
+    res = {"iteration": []}
     fused_seen = False
+    # every launch of the profiled fused iteration (run prologue included),
+    # until the first separate-kernel attractive launch
+    for row in table:
+        if row["kernel"] == "k_attractive" and any(
+                r["kernel"] == "k_forces" for r in res["iteration"]):
+            break
+        res["iteration"].append({
+            "kernel": row["kernel"],
+            "us": row.get("gpu__time_duration.sum", 0.0) * 1e-3,
+            "dram_mb": (row.get("dram__bytes_read.sum", 0.0)
+                        + row.get("dram__bytes_write.sum", 0.0)) * 1e-6})
     for row in table:
         k = row["kernel"]
         if k == "k_forces" and not fused_seen:
@@ -580,6 +591,7 @@ def ours_arm(args, rank, world):
     ncu = None
     if args.ncu and world == 1:
         ncu = summarize_ncu(ncu_profile(args))
+    ncu_iteration = ncu.pop("iteration", None) if ncu else None
     if ncu:
         for name, row in ncu.items():
             if name in kernels:
@@ -643,6 +655,7 @@ def ours_arm(args, rank, world):
         "config": config_dict(args, n, nnz),
         "e2e": e2e, "gpu_launches": launches,
         "roofline": roof, "kernels": kernels, "stage_ms": stage_ms,
+        "ncu_iteration": ncu_iteration,
         "clocks": clk.summary(), "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

@@ -486,6 +486,16 @@ int bh_permute_csr_f64(const int64_t *row_ptr, const int32_t *col,
  * x: (n, d) float32 row-major, d <= 64, k <= 128. */
 int bh_knn(const float *x, int64_t n, int64_t d, int64_t k, int64_t *out_idx,
            float *out_sqd, bh_stream_t stream);
+/* Any D and k (the same semantics and results as bh_knn; slower): the
+ * query's columns streamed in chunks, the running top-k in caller scratch of
+ * bh_knn_general_workspace_bytes(n, k) bytes. */
+size_t bh_knn_general_workspace_bytes(int64_t n, int64_t k);
+int bh_knn_general(const float *x, int64_t n, int64_t d, int64_t k,
+                   int64_t *out_idx, float *out_sqd, void *ws,
+                   size_t ws_bytes, bh_stream_t stream);
+int bh_knn_general_f64(const double *x, int64_t n, int64_t d, int64_t k,
+                       int64_t *out_idx, double *out_sqd, void *ws,
+                       size_t ws_bytes, bh_stream_t stream);
 /* f64 run mode: float64 data, distances returned as float64. */
 int bh_knn_f64(const double *x, int64_t n, int64_t d, int64_t k,
                int64_t *out_idx, double *out_sqd, bh_stream_t stream);

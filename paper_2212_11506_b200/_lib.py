@@ -130,6 +130,10 @@ SIGNATURES = {
     "bh_pad_csr_size": ([_P, _I64, _P, _P, _P, _SZ, _P], C.c_int),
     "bh_pad_csr_fill": ([_P, _P, _P, _I64, _P, _P, _P, _P], C.c_int),
     "bh_knn": ([_P, _I64, _I64, _I64, _P, _P, _P], C.c_int),
+    "bh_knn_general_workspace_bytes": ([_I64, _I64], _SZ),
+    "bh_knn_general": ([_P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P], C.c_int),
+    "bh_knn_general_f64": ([_P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P],
+                           C.c_int),
     "bh_gather_rows": ([_P, _P, _I64, C.c_int, _P, _P], C.c_int),
     "bh_scatter_rows": ([_P, _P, _I64, C.c_int, _P, _P], C.c_int),
     "bh_invert_perm": ([_P, _I64, _P, _P], C.c_int),

@@ -4,7 +4,7 @@
 // kept on the device (bh_part_t) so captured CUDA graphs survive a
 // re-balance.  The reference has no counterpart (its only parallel axis is
 // numba prange over points, optimizer.py:273-286, forces.py:89).
-#include "common.cuh"
+#include "forces.cuh"
 
 namespace bh {
 
@@ -89,46 +89,43 @@ __global__ void k_unpack(const E *__restrict__ gbuf, int64_t cap,
     }
 }
 
-// Z partial of each 128-slot block of the share (fixed order: a butterfly
-// per warp, then the warps in order), the same blocks on any number of GPUs;
-// with z_out, the last CTA folds all blocks (fixed_sum, one GPU).
-__global__ void __launch_bounds__(kAlign)
+// Z partial of each 128-slot block of the share, in a fixed order (one warp
+// per block: lane l sums slots l, l+32, l+64, l+96 of it, then a butterfly)
+// -- the same blocks and sums on any number of GPUs; with z_out (one GPU)
+// the last CTA folds all blocks (cta_fold, as bh_sum_partials does after
+// the all-reduce on several).
+__global__ void __launch_bounds__(kFoldThreads)
 k_zsum(const double *__restrict__ zpart, const bh_part_t *__restrict__ p,
        int64_t n, double *__restrict__ zblock, double *__restrict__ z_out,
        unsigned *__restrict__ ticket) {
-    __shared__ double s_w[kAlign / 32];
+    __shared__ double s_w[kFoldThreads / 32];
     __shared__ bool s_last;
     const int64_t lo = p->lo, hi = p->hi;
-    const int64_t nb = (hi - lo + kAlign - 1) / kAlign;
-    const int64_t b = lo / kAlign + blockIdx.x;
-    const bool mine = (int64_t)blockIdx.x < nb;
-    if (mine) {
-        const int64_t s = b * kAlign + threadIdx.x;
-        const double v = s < hi ? zpart[s] : 0.0;
-        const double w = warp_sum(v);
-        if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = w;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int i = 0; i < kAlign / 32; i++) t = __dadd_rn(t, s_w[i]);
-            zblock[b] = t;
+    const int64_t b0 = lo / kAlign, nb = (hi - lo + kAlign - 1) / kAlign;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kW = kFoldThreads / 32;
+    for (int64_t q = (int64_t)blockIdx.x * kW + warp; q < nb;
+         q += (int64_t)gridDim.x * kW) {
+        const int64_t base = (b0 + q) * kAlign;
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < kAlign / 32; r++) {
+            const int64_t s = base + r * 32 + lane;
+            if (s < hi) v = __dadd_rn(v, zpart[s]);
         }
+        v = warp_sum(v);
+        if (lane == 0) zblock[b0 + q] = v;
     }
     if (!z_out) return;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last || threadIdx.x >= 32) return;
     __threadfence();
-    const int64_t all = (n + kAlign - 1) / kAlign;
-    double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < all; i += 32)
-        acc = __dadd_rn(acc, __ldcg(&zblock[i]));
-    acc = warp_sum(acc);
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const double tot = cta_fold(zblock, (n + kAlign - 1) / kAlign, s_w);
     if (threadIdx.x == 0) {
-        *z_out = acc;
+        *z_out = tot;
         *ticket = 0;
     }
 }
@@ -260,9 +257,11 @@ extern "C" int bh_step_zsum(const double *zpart, const bh_part_t *part,
                             bh_stream_t stream) {
     BH_REQUIRE(ws_bytes >= 256, "zsum workspace too small");
     BH_REQUIRE(max_points >= 1 && max_points <= n, "bad max_points");
-    const int grid = (int)((max_points + kAlign - 1) / kAlign);
-    k_zsum<<<grid, kAlign, 0, bh_cs(stream)>>>(zpart, part, n, zblock, z_out,
-                                               (unsigned *)ws);
+    const int64_t blocks = (max_points + kAlign - 1) / kAlign;
+    int grid = (int)((blocks + kFoldThreads / 32 - 1) / (kFoldThreads / 32));
+    if (grid > kSMs * 4) grid = kSMs * 4;
+    k_zsum<<<grid, kFoldThreads, 0, bh_cs(stream)>>>(zpart, part, n, zblock,
+                                                     z_out, (unsigned *)ws);
     BH_CHECK_LAUNCH("k_zsum");
     return BH_OK;
 }

@@ -379,10 +379,11 @@ k_repulsive(const RepArgs A) {
 
     rep_block<D, COUNT, QUERY, SC>(A, blockIdx.x, gridDim.x);
 }
-// Sum of gathered per-CTA Z partials into *out (one warp, fixed order).
-__global__ void k_fixed_sum(const double *__restrict__ x, int64_t n,
-                            double *__restrict__ out) {
-    double s = fixed_sum(x, n);
+// Sum of gathered Z partials into *out (one CTA, cta_fold).
+__global__ void __launch_bounds__(kFoldThreads)
+k_fixed_sum(const double *__restrict__ x, int64_t n, double *__restrict__ out) {
+    __shared__ double s_w[kFoldThreads / 32];
+    const double s = cta_fold(x, n, s_w);
     if (threadIdx.x == 0) *out = s;
 }
 
@@ -694,7 +695,7 @@ extern "C" int bh_repulsive(const bh_tree_t *t, const bh_bounds_t *bounds,
 
 extern "C" int bh_sum_partials(const double *x, int64_t n, double *out,
                                bh_stream_t stream) {
-    k_fixed_sum<<<1, 32, 0, bh_cs(stream)>>>(x, n, out);
+    k_fixed_sum<<<1, kFoldThreads, 0, bh_cs(stream)>>>(x, n, out);
     BH_CHECK_LAUNCH("k_fixed_sum");
     return BH_OK;
 }

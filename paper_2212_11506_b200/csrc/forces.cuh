@@ -28,6 +28,27 @@ __device__ __forceinline__ double fixed_sum(const double *x, int64_t n) {
     return warp_sum(s);
 }
 
+// Deterministic fold of n f64 partials by one CTA of kFoldThreads: thread t
+// sums x[t], x[t + kFoldThreads], ... in order, a butterfly per warp, then
+// the warps in order.  The engine's Z total on one GPU (bh_step_zsum's
+// tail) and after the all-reduce on several (bh_sum_partials) -- the same
+// fold, so Z is bitwise independent of the GPU count.  Result valid in
+// thread 0.
+constexpr int kFoldThreads = 256;
+__device__ __forceinline__ double cta_fold(const double *x, int64_t n,
+                                           double *s_w /* kFoldThreads/32 */) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += kFoldThreads)
+        s = __dadd_rn(s, __ldcg(&x[i]));
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kFoldThreads / 32; w++) t = __dadd_rn(t, s_w[w]);
+    return t;
+}
+
 // The row range of a CSR sweep: explicit, or the engine's share (bh_part_t):
 // rows [part->lo, part->split) when which == 0 (the side-stream sweep),
 // [part->split, part->hi) otherwise.

@@ -80,9 +80,116 @@ k_knn(const T *__restrict__ x, int64_t n, int d, int k,
     }
 }
 
+// Any D, any k (bh_knn_general): the same arithmetic and insertion rule,
+// with the query's columns streamed in chunks of kKnnChunk (a tile of 32
+// candidate rows per chunk in shared memory, one f64 partial sum per
+// candidate in registers) and the running top-k in caller scratch (global,
+// L1/L2 resident per thread).  A candidate whose partial sum already
+// exceeds the k-th distance after a chunk is dropped from the remaining
+// chunks (the sum is monotone).
+constexpr int kKnnChunk = 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kKnnThreads)
+k_knn_general(const T *__restrict__ x, int64_t n, int d, int k,
+              int64_t *__restrict__ out_idx, T *__restrict__ out_sqd,
+              double *__restrict__ ws_d, int32_t *__restrict__ ws_i) {
+    __shared__ double s_c[kKnnTile][kKnnChunk + 1];
+    const int64_t i = blockIdx.x * (int64_t)kKnnThreads + threadIdx.x;
+    const bool ok = i < n;
+    double *bd = ws_d + (ok ? i : 0) * (int64_t)k;
+    int32_t *bi = ws_i + (ok ? i : 0) * (int64_t)k;
+    if (ok)
+        for (int t = 0; t < k; t++) {
+            bd[t] = INFINITY;
+            bi[t] = -1;
+        }
+    double thr = INFINITY;
+    for (int64_t j0 = 0; j0 < n; j0 += kKnnTile) {
+        const int nb = (n - j0) < kKnnTile ? (int)(n - j0) : kKnnTile;
+        double acc[kKnnTile];
+#pragma unroll
+        for (int r = 0; r < kKnnTile; r++) acc[r] = 0.0;
+        for (int c0 = 0; c0 < d; c0 += kKnnChunk) {
+            const int nc = (d - c0) < kKnnChunk ? d - c0 : kKnnChunk;
+            __syncthreads();
+            for (int e = threadIdx.x; e < kKnnTile * kKnnChunk; e += kKnnThreads) {
+                const int r = e / kKnnChunk, c = e % kKnnChunk;
+                const int64_t j = j0 + r;
+                s_c[r][c] = (j < n && c < nc) ? (double)x[j * d + c0 + c] : 0.0;
+            }
+            __syncthreads();
+            if (!ok) continue;
+            for (int c = 0; c < nc; c++) {
+                const double qc = (double)x[i * d + c0 + c];
+#pragma unroll
+                for (int r = 0; r < kKnnTile; r++) {
+                    const double diff = __dsub_rn(qc, s_c[r][c]);
+                    acc[r] = __dadd_rn(acc[r], __dmul_rn(diff, diff));
+                }
+            }
+        }
+        if (!ok) continue;
+        for (int r = 0; r < nb; r++) {
+            const int64_t j = j0 + r;
+            const double a = acc[r];
+            if (j == i || !(a < thr)) continue;
+            int pos = k - 1;
+            while (pos > 0 && a < bd[pos - 1]) {
+                bd[pos] = bd[pos - 1];
+                bi[pos] = bi[pos - 1];
+                pos--;
+            }
+            bd[pos] = a;
+            bi[pos] = (int32_t)j;
+            thr = bd[k - 1];
+        }
+    }
+    if (ok)
+        for (int t = 0; t < k; t++) {
+            out_idx[i * k + t] = bi[t];
+            out_sqd[i * k + t] = (T)bd[t];
+        }
+}
+
 }  // namespace bh
 
 using namespace bh;
+
+extern "C" size_t bh_knn_general_workspace_bytes(int64_t n, int64_t k) {
+    return bh_align(sizeof(double) * n * k) + bh_align(sizeof(int32_t) * n * k);
+}
+
+template <typename T>
+static int knn_general_impl(const T *x, int64_t n, int64_t d, int64_t k,
+                            int64_t *out_idx, T *out_sqd, void *ws,
+                            size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(k >= 1 && k <= n - 1, "k must be in [1, %lld], got %lld",
+               (long long)(n - 1), (long long)k);
+    BH_REQUIRE(d >= 1, "need at least one column");
+    BH_REQUIRE(ws_bytes >= bh_knn_general_workspace_bytes(n, k),
+               "kNN workspace too small");
+    double *wd = (double *)ws;
+    int32_t *wi = (int32_t *)((char *)ws + bh_align(sizeof(double) * n * k));
+    k_knn_general<T><<<bh_blocks(n, kKnnThreads), kKnnThreads, 0,
+                       bh_cs(stream)>>>(x, n, (int)d, (int)k, out_idx,
+                                        out_sqd, wd, wi);
+    BH_CHECK_LAUNCH("k_knn_general");
+    return BH_OK;
+}
+
+extern "C" int bh_knn_general(const float *x, int64_t n, int64_t d, int64_t k,
+                              int64_t *out_idx, float *out_sqd, void *ws,
+                              size_t ws_bytes, bh_stream_t stream) {
+    return knn_general_impl(x, n, d, k, out_idx, out_sqd, ws, ws_bytes, stream);
+}
+
+extern "C" int bh_knn_general_f64(const double *x, int64_t n, int64_t d,
+                                  int64_t k, int64_t *out_idx, double *out_sqd,
+                                  void *ws, size_t ws_bytes,
+                                  bh_stream_t stream) {
+    return knn_general_impl(x, n, d, k, out_idx, out_sqd, ws, ws_bytes, stream);
+}
 
 template <typename T>
 static int knn_impl(const T *x, int64_t n, int64_t d, int64_t k,

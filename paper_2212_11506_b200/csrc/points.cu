@@ -231,22 +231,22 @@ __device__ __forceinline__ double2 shifted(double2 p, const bh_bounds_t *b) {
 // has no jumps between consecutive points.
 template <int BITS, typename U>
 __device__ __forceinline__ U hilbert_key(U x, U y) {
+    // Branch-free form of the walk: the rotations and reflections applied so
+    // far are a state (swap, comp) acting on the ORIGINAL bits of each level:
+    // (xt, yt) = (swap ? (by, bx) : (bx, by)) ^ comp, digit = (3 xt) ^ yt,
+    // and a level with yt == 0 toggles swap and, when xt == 1, comp.
     constexpr int H = BITS / 2;
-    constexpr U full = (U)((1ull << H) - 1ull);
+    uint32_t swap = 0, comp = 0;
     U d = 0;
 #pragma unroll
     for (int l = H - 1; l >= 0; l--) {
-        const U rx = (x >> l) & 1u, ry = (y >> l) & 1u;
-        d = (d << 2) | ((3u * rx) ^ ry);
-        if (ry == 0) {
-            if (rx == 1) {
-                x = full - x;
-                y = full - y;
-            }
-            const U t = x;
-            x = y;
-            y = t;
-        }
+        const uint32_t bx = (uint32_t)(x >> l) & 1u, by = (uint32_t)(y >> l) & 1u;
+        const uint32_t t = (bx ^ by) & swap;
+        const uint32_t xt = bx ^ t ^ comp, yt = by ^ t ^ comp;
+        d = (d << 2) | (U)(((xt << 1) | xt) ^ yt);
+        const uint32_t z = yt ^ 1u;
+        swap ^= z;
+        comp ^= xt & z;
     }
     return d;
 }

@@ -15,8 +15,10 @@ from ._lib import call, ptr, stream
 from .affinity import NeighborGraph
 
 
-MAX_K = 128  # bh_knn: per-thread candidate list (csrc/knn.cu kKnnMaxK)
-MAX_D = 64   # bh_knn: the query row held in registers
+# bh_knn (query row in registers, top-k list in local memory) covers
+# k <= 128 and D <= 64; bh_knn_general any k and D (slower)
+MAX_K = 128
+MAX_D = 64
 
 
 def knn_exact(x, k: int) -> NeighborGraph:
@@ -29,15 +31,14 @@ def knn_exact(x, k: int) -> NeighborGraph:
     n, d = data.shape
     if not 1 <= k <= n - 1:
         raise ValueError(f"k must be in [1, {n - 1}], got {k}")
-    if k > MAX_K or d > MAX_D:
-        raise ValueError(
-            f"the GPU exact kNN supports k <= {MAX_K} (perplexity < "
-            f"{(MAX_K + 1) / 3:.0f}) and D <= {MAX_D}; got k={k}, D={d}. "
-            "Pass a precomputed graph (run(..., knn=NeighborGraph) or "
-            "--knn graph.npz), e.g. the reference's knn_exact, or reduce D "
-            "(PCA) first")
     idx = torch.empty((n, k), dtype=torch.int64, device=data.device)
     sqd = torch.empty((n, k), dtype=dt, device=data.device)
-    call(_lib.fn("bh_knn", dt), ptr(data), n, d, k, ptr(idx), ptr(sqd),
-         stream())
+    if k <= MAX_K and d <= MAX_D:
+        call(_lib.fn("bh_knn", dt), ptr(data), n, d, k, ptr(idx), ptr(sqd),
+             stream())
+    else:  # any D / k: columns in chunks, the top-k list in scratch
+        lib = _lib.load()
+        ws = _lib.workspace(lib.bh_knn_general_workspace_bytes(n, k))
+        call(_lib.fn("bh_knn_general", dt), ptr(data), n, d, k, ptr(idx),
+             ptr(sqd), ptr(ws), ws.numel(), stream())
     return NeighborGraph(idx, sqd)

@@ -27,14 +27,18 @@ from paper_2212_11506_b200.dist import (POINTS_PER_PARTIAL, W_POINT,  # noqa: E4
 
 
 def fixed_sum(x):
-    """Host mirror of the device fixed_sum: 32 lane-strided sequential
-    partials, then an xor butterfly."""
-    lanes = np.zeros(32)
+    """Host mirror of the device cta_fold (forces.cuh): 256 thread-strided
+    sequential partials, an xor butterfly per warp, the 8 warps in order."""
+    th = np.zeros(256)
     for i, v in enumerate(x):
-        lanes[i % 32] = lanes[i % 32] + v
-    for o in (16, 8, 4, 2, 1):
-        lanes = np.array([lanes[l] + lanes[l ^ o] for l in range(32)])
-    return lanes[0]
+        th[i % 256] = th[i % 256] + v
+    tot = 0.0
+    for w in range(8):
+        lanes = th[32 * w:32 * (w + 1)].copy()
+        for o in (16, 8, 4, 2, 1):
+            lanes = np.array([lanes[l] + lanes[l ^ o] for l in range(32)])
+        tot = tot + lanes[0]
+    return tot
 
 
 def problem():

@@ -302,6 +302,22 @@ def test_knn_exact_vs_reference(bh):
                                   golden("c0_run")["indices"].astype(np.int64))
 
 
+@pytest.mark.parametrize("n,d,k", [(600, 100, 40), (700, 12, 200),
+                                   (300, 784, 299)])
+def test_knn_general_any_d_and_k(bh, oracle, n, d, k):
+    """Beyond bh_knn's D <= 64 / k <= 128 (e.g. perplexity 50+, raw
+    784-pixel images): bh_knn_general, the same semantics (f64 column-order
+    sums, ties -> lower id) against the oracle's knn.py restatement."""
+    from paper_2212_11506_b200.knn import knn_exact
+    rng = np.random.default_rng(d)
+    x = rng.integers(0, 4, (n, d)).astype(np.float32)  # many exact ties
+    for dt in (np.float32, np.float64):
+        g = knn_exact(x.astype(dt), k)
+        idx, sqd = oracle.knn_exact(x.astype(dt), k)
+        np.testing.assert_array_equal(g.indices.cpu().numpy(), idx)
+        np.testing.assert_array_equal(g.sq_distances.cpu().numpy(), sqd)
+
+
 # --- optimiser ------------------------------------------------------------
 
 def test_gradient_step_trajectory_vs_reference(bh):
