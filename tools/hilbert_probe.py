@@ -110,6 +110,40 @@ def main():
         if ref is None:
             ref = r
         out[name + "_bitwise_same"] = bool(torch.equal(r, ref))
+    # union size of 16-point warps: every warp holds 16 Hilbert-consecutive
+    # points twice (2N lanes), so its walk is the union of 16 points' walks;
+    # half of that kernel's time estimates a half-warp traversal's
+    import ctypes as C
+    import numpy as np
+    h = hil.cpu().numpy()
+    m = (n // 16) * 16
+    dup = np.concatenate([h[:m].reshape(-1, 16), h[:m].reshape(-1, 16)],
+                         axis=1).reshape(-1)
+    q16 = torch.from_numpy(np.ascontiguousarray(dup)).to(eng.dev)
+    part2 = torch.tensor([0, q16.numel(), q16.numel(), 1], dtype=torch.int64,
+                         device=eng.dev)
+    fake = type(t.struct).from_buffer_copy(t.struct)
+    fake.n_points = q16.numel()
+    ws2 = bh.quadtree._lib.workspace(
+        bh.quadtree._lib.load().bh_repulsive_workspace_bytes(q16.numel()))
+
+    def run16():
+        call("bh_step_forces", C.byref(fake), ptr(eng.bounds), 0.5, ptr(eng.y),
+             ptr(eng.rank_of), ptr(q16), ptr(part2), q16.numel(), 1,
+             ptr(eng.rep), ptr(eng.zpart), ptr(ws2), ws2.numel(), ptr(eng.rp),
+             ptr(eng.col), ptr(eng.val), 1, ptr(eng.sched), ptr(eng.attr),
+             stream())
+
+    run16()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    c = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.reps):
+        run16()
+    c.record()
+    c.synchronize()
+    out["hilbert_16pt_unions_half_time"] = a.elapsed_time(c) / args.reps / 2
     print(json.dumps(out), flush=True)
 
 
