@@ -530,13 +530,18 @@ def ours_arm(args, rank, world):
     lo_ = eng.tree.level_off.cpu().numpy()
     n_nodes = int(lo_[int(lo_[-1])])
     nnz_pad = int(eng.rp[-1].item())
-    y_end = e.y.cpu().numpy() if rank == 0 else None
+    y_end = e.y.cpu().numpy()
+    # --- e2e through the public API with host buffers (every rank: on
+    #     several GPUs the engines exchange through NCCL)
+    runs = [e2e_run(bh, prob, cfg, args, rank, world)
+            for _ in range(max(1, args.e2e_repeats))]
+    host_state = e2e_host(bh, p, cfg, y_end, args, rank, world)
     if rank != 0:
         return
     value = args.steps / (ms * 1e-3)
     stage_ms = {s: 1e3 * timings.total(s) / max(1, timings.calls(s))
                 for s in ("tree", "summarize", "attractive", "repulsive",
-                          "update", "comm")}
+                          "update", "comm", "relabel")}
     if timings_f.calls("forces"):
         stage_ms["forces"] = 1e3 * timings_f.total("forces") / timings_f.calls("forces")
     for s_, key in (("forces", "force_phase_pipelined"),
@@ -627,12 +632,11 @@ def ours_arm(args, rank, world):
             "leaf_points_per_point": cnt[2] / n}
 
     # --- e2e through the public API with host buffers
-    runs = [e2e_run(bh, prob, cfg, args) for _ in range(max(1, args.e2e_repeats))]
     vals = sorted(r["value"] for r in runs)
     e2e = dict(runs[len(runs) // 2], value=vals[len(vals) // 2],
                repeats=[r["value"] for r in runs],
                summary=f"median of {len(runs)} end-to-end runs")
-    e2e["per_step_host_state"] = e2e_host(bh, p, cfg, y_end, args)
+    e2e["per_step_host_state"] = host_state
 
     # --- CPU oracle on the host cores, bounded sample from the same state
     cpu = None
@@ -661,7 +665,24 @@ def ours_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def e2e_run(bh, prob, cfg, args):
+def _shard(rank, world):
+    if world == 1:
+        return None
+    from paper_2212_11506_b200.dist import Shard
+    return Shard(rank, world)
+
+
+def _max_over_ranks(seconds, world):
+    if world == 1:
+        return seconds
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([seconds], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def e2e_run(bh, prob, cfg, args, rank=0, world=1):
     """End to end through the public optimiser API with HOST inputs, the
     way a user runs it: the symmetric P (CSR) and Y0 in pinned host memory
     are uploaded, the engine is built (row padding, graph capture) and runs
@@ -684,7 +705,7 @@ def e2e_run(bh, prob, cfg, args):
         e = bh.embedding_from(y0)
         torch.cuda.synchronize()
         t1 = tick()
-        eng = bh.Engine(p, e, cfg)
+        eng = bh.Engine(p, e, cfg, shard=_shard(rank, world))
         torch.cuda.synchronize()
         t2 = tick()
         eng.run(iters)
@@ -692,7 +713,7 @@ def e2e_run(bh, prob, cfg, args):
         t3 = tick()
         y_out = e.y.cpu()
         torch.cuda.synchronize()
-        dt = tick() - t0
+        dt = _max_over_ranks(tick() - t0, world)
     h2d = sum(int(t.numel() * t.element_size()) for t in (ro, co, va, y0))
     d2h = int(y_out.numel() * y_out.element_size())
     sched = 96 * math.ceil(iters / cfg.graph_chunk)
@@ -710,7 +731,7 @@ def e2e_run(bh, prob, cfg, args):
             "clocks": clk.summary()}
 
 
-def e2e_host(bh, p, cfg, y_host, args):
+def e2e_host(bh, p, cfg, y_host, args, rank=0, world=1):
     """gradient_step-style use: the embedding state lives on the host and
     every step uploads it, runs one iteration and reads it back."""
     import torch
@@ -718,7 +739,7 @@ def e2e_host(bh, p, cfg, y_host, args):
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     hy, hv, hg = pin(y_host), pin(np.zeros_like(y_host)), pin(np.ones_like(y_host))
     e = bh.embedding_from(y_host)
-    eng = bh.Engine(p, e, cfg, schedule=True)
+    eng = bh.Engine(p, e, cfg, schedule=True, shard=_shard(rank, world))
     steps = max(1, min(args.steps, args.e2e_steps))
 
     def one():
@@ -737,7 +758,7 @@ def e2e_host(bh, p, cfg, y_host, args):
     for _ in range(steps):
         one()
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    dt = _max_over_ranks(time.perf_counter() - t0, world)
     bytes_state = 3 * n * 2 * y_host.dtype.itemsize
     return {"value": steps / dt, "unit": "it/s",
             "h2d_bytes_per_step": bytes_state, "d2h_bytes_per_step": bytes_state,
