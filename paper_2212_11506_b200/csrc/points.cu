@@ -9,7 +9,7 @@
 
 #include <type_traits>
 
-#include "common.cuh"
+#include "keys.cuh"
 
 namespace bh {
 
@@ -18,25 +18,6 @@ constexpr int kPtThreads = 256;
 #define BH_PT_BLOCKS_PER_SM 4  // update 26 us vs 28 (8), 34 (16)
 #endif
 constexpr int kPtMaxBlocks = kSMs * BH_PT_BLOCKS_PER_SM;
-
-__device__ __forceinline__ uint32_t spread16(uint32_t x) {
-    x &= 0xFFFFu;
-    x = (x | (x << 8)) & 0x00FF00FFu;
-    x = (x | (x << 4)) & 0x0F0F0F0Fu;
-    x = (x | (x << 2)) & 0x33333333u;
-    x = (x | (x << 1)) & 0x55555555u;
-    return x;
-}
-
-__device__ __forceinline__ uint64_t spread32(uint64_t m) {  // _spread_bits
-    m &= 0x00000000FFFFFFFFull;
-    m = (m | (m << 16)) & 0x0000FFFF0000FFFFull;
-    m = (m | (m << 8)) & 0x00FF00FF00FF00FFull;
-    m = (m | (m << 4)) & 0x0F0F0F0F0F0F0F0Full;
-    m = (m | (m << 2)) & 0x3333333333333333ull;
-    m = (m | (m << 1)) & 0x5555555555555555ull;
-    return m;
-}
 
 // compute_bounds (quadtree.py:145-153) from exact f32 extrema, plus the
 // Morton constants of _morton_kernel (quadtree.py:179-181).
@@ -214,43 +195,6 @@ k_bounds(const p2_t<T> *__restrict__ y, int64_t n, int code_bits,
     }
 }
 
-// y - shift in the run precision (gradient_step's re-centering)
-__device__ __forceinline__ float2 shifted(float2 p, const bh_bounds_t *b) {
-    return make_float2(__fsub_rn(p.x, b->shift0), __fsub_rn(p.y, b->shift1));
-}
-__device__ __forceinline__ double2 shifted(double2 p, const bh_bounds_t *b) {
-    return make_double2(__dsub_rn(p.x, b->shift0_f64),
-                        __dsub_rn(p.y, b->shift1_f64));
-}
-
-// Hilbert index of the quantised cell (m0, m1), BITS/2 bits per dimension,
-// the classic rotate-and-reflect walk from the top bit.  The top 2d bits of
-// the index name the depth-d quadtree cell of the point (a bijection at
-// every level), so the canonical tree over Hilbert keys has exactly the
-// Morton tree's cells -- only siblings are ordered along the curve, which
-// has no jumps between consecutive points.
-template <int BITS, typename U>
-__device__ __forceinline__ U hilbert_key(U x, U y) {
-    // Branch-free form of the walk: the rotations and reflections applied so
-    // far are a state (swap, comp) acting on the ORIGINAL bits of each level:
-    // (xt, yt) = (swap ? (by, bx) : (bx, by)) ^ comp, digit = (3 xt) ^ yt,
-    // and a level with yt == 0 toggles swap and, when xt == 1, comp.
-    constexpr int H = BITS / 2;
-    uint32_t swap = 0, comp = 0;
-    U d = 0;
-#pragma unroll
-    for (int l = H - 1; l >= 0; l--) {
-        const uint32_t bx = (uint32_t)(x >> l) & 1u, by = (uint32_t)(y >> l) & 1u;
-        const uint32_t t = (bx ^ by) & swap;
-        const uint32_t xt = bx ^ t ^ comp, yt = by ^ t ^ comp;
-        d = (d << 2) | (U)(((xt << 1) | xt) ^ yt);
-        const uint32_t z = yt ^ 1u;
-        swap ^= z;
-        comp ^= xt & z;
-    }
-    return d;
-}
-
 template <int BITS, typename T, bool HILBERT = false>
 __global__ void __launch_bounds__(kPtThreads)
 k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
@@ -268,17 +212,8 @@ k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
             p = shifted(p, b);
             y[i] = p;
         }
-        double q0 = __dmul_rn(__dsub_rn((double)p.x, root0), scale);
-        double q1 = __dmul_rn(__dsub_rn((double)p.y, root1), scale);
-        if constexpr (BITS == 32) {
-            uint32_t m0 = __double2uint_rz(q0), m1 = __double2uint_rz(q1);
-            codes[i] = HILBERT ? hilbert_key<32>(m0, m1)
-                               : spread16(m0) | (spread16(m1) << 1);
-        } else {
-            uint64_t m0 = __double2ull_rz(q0), m1 = __double2ull_rz(q1);
-            codes[i] = HILBERT ? hilbert_key<64>(m0, m1)
-                               : spread32(m0) | (spread32(m1) << 1);
-        }
+        codes[i] = point_key<BITS, HILBERT>((double)p.x, (double)p.y, root0,
+                                             root1, scale);
     }
 }
 

@@ -40,9 +40,17 @@ struct SortCfg {
 // the whole chain is kernel-to-kernel (PDL).  Counts accumulate into one of
 // two buffers chosen by a call epoch; the last CTA publishes them to `hist`,
 // and zeroes the other buffer for the next call.
+// Where the histogram pass gets its keys (a functor: the key array of
+// bh_sort; a fused key computation was measured and rejected).
 template <typename K>
+struct KeysIn {
+    const K *__restrict__ keys;
+    __device__ __forceinline__ K operator()(int64_t i) const { return keys[i]; }
+};
+
+template <typename K, typename Src = KeysIn<K>>
 __global__ void __launch_bounds__(256)
-k_sort_hist(const K *__restrict__ keys, int64_t n, int passes,
+k_sort_hist(const Src src, int64_t n, int passes,
             uint32_t *__restrict__ hist, uint32_t *__restrict__ acc2,
             uint32_t *__restrict__ epoch, unsigned *__restrict__ ticket,
             uint32_t *__restrict__ zero, int64_t zero_words) {
@@ -68,7 +76,7 @@ k_sort_hist(const K *__restrict__ keys, int64_t n, int passes,
         const int cnt = (int)min((int64_t)kRun, n - s);
         K kk[kRun];
 #pragma unroll
-        for (int j = 0; j < kRun; j++) kk[j] = j < cnt ? keys[s + j] : K(0);
+        for (int j = 0; j < kRun; j++) kk[j] = j < cnt ? src(s + j) : K(0);
         for (int p = 0; p < passes; p++) {
             unsigned cur = (unsigned)(kk[0] >> (8 * p)) & 0xFFu, run = 1;
 #pragma unroll
@@ -266,10 +274,10 @@ static SortLayout sort_layout(int64_t n, int key_bits) {
     return L;
 }
 
-template <typename K>
+template <typename K, typename Src = KeysIn<K>>
 static int sort_impl(const K *keys, const uint32_t *vals, int64_t n,
                      int key_bits, K *out_keys, uint32_t *out_vals, void *ws,
-                     size_t ws_bytes, cudaStream_t st) {
+                     size_t ws_bytes, cudaStream_t st, Src src) {
     BH_REQUIRE(n >= 0 && n < (int64_t)kValMask, "sort size out of range");
     BH_REQUIRE(key_bits >= 1 && key_bits <= 8 * (int)sizeof(K),
                "key_bits out of range");
@@ -287,7 +295,7 @@ static int sort_impl(const K *keys, const uint32_t *vals, int64_t n,
     // tile counters and look-back status are contiguous: [ctr, status)
     const int64_t zero_words = (int64_t)((L.status - L.ctr) / 4 +
                                          (size_t)256 * L.tiles * L.passes);
-    BH_LAUNCH("k_sort_hist", k_sort_hist<K>, hb, 256, 0, st, keys, n,
+    BH_LAUNCH("k_sort_hist", (k_sort_hist<K, Src>), hb, 256, 0, st, src, n,
               L.passes, hist, (uint32_t *)(w + L.acc), misc, misc + 1, ctr,
               zero_words);
     K *kb[2] = {(K *)(w + L.keys_a), (K *)(w + L.keys_b)};
@@ -319,12 +327,13 @@ extern "C" int bh_sort_pairs(const void *keys, const uint32_t *vals, int64_t n,
                              uint32_t *sorted_vals, void *ws, size_t ws_bytes,
                              bh_stream_t stream) {
     if (key_bits <= 32)
-        return sort_impl<uint32_t>((const uint32_t *)keys, vals, n, key_bits,
-                                   (uint32_t *)sorted_keys, sorted_vals, ws,
-                                   ws_bytes, bh_cs(stream));
-    return sort_impl<uint64_t>((const uint64_t *)keys, vals, n, key_bits,
-                               (uint64_t *)sorted_keys, sorted_vals, ws,
-                               ws_bytes, bh_cs(stream));
+        return sort_impl((const uint32_t *)keys, vals, n, key_bits,
+                         (uint32_t *)sorted_keys, sorted_vals, ws, ws_bytes,
+                         bh_cs(stream),
+                         KeysIn<uint32_t>{(const uint32_t *)keys});
+    return sort_impl((const uint64_t *)keys, vals, n, key_bits,
+                     (uint64_t *)sorted_keys, sorted_vals, ws, ws_bytes,
+                     bh_cs(stream), KeysIn<uint64_t>{(const uint64_t *)keys});
 }
 
 extern "C" int bh_sort(const void *keys, int64_t n, int key_bits,
