@@ -541,9 +541,14 @@ def ours_arm(args, rank, world):
     value = args.steps / (ms * 1e-3)
     stage_ms = {s: 1e3 * timings.total(s) / max(1, timings.calls(s))
                 for s in ("tree", "summarize", "attractive", "repulsive",
-                          "update", "comm", "relabel")}
+                          "update", "comm", "relabel", "iteration")}
     if timings_f.calls("forces"):
         stage_ms["forces"] = 1e3 * timings_f.total("forces") / timings_f.calls("forces")
+    if timings_p.calls("iteration"):
+        # the timed region's pipeline, evented: the iteration span and the
+        # remainder of the step (graph launch gaps, relabels, chunk syncs)
+        stage_ms["iteration_pipelined"] = (1e3 * timings_p.total("iteration")
+                                           / timings_p.calls("iteration"))
     for s_, key in (("forces", "force_phase_pipelined"),
                     ("attractive", "side_sweep_span")):
         if timings_p.calls(s_):

@@ -46,7 +46,9 @@ STAGES = ("knn", "bsp", "tree", "summarize", "attractive", "repulsive",
 # the stages a report lists: the reference's, plus the fused force launch
 REPORT_STAGES = STAGES + ("forces",)
 # "forces": the fused attractive + repulsive launch (Engine.fuse_timed)
-EXTRA_STAGES = ("comm", "relabel", "forces")
+# "iteration": start of the key pass to the end of the update (and the Y
+# exchange), one event pair per iteration
+EXTRA_STAGES = ("comm", "relabel", "forces", "iteration")
 MOMENTUM_SWITCH_ITER = 250
 PRECISIONS = ("f32", "f64")
 
@@ -145,6 +147,24 @@ class Embedding:
 
     def numpy(self) -> np.ndarray:
         return self.y.cpu().numpy()
+
+    def save(self, path) -> None:
+        """Checkpoint the optimiser state (y, velocity, gains, iteration,
+        seed) -- what a resumed run needs (the reference has
+        no checkpoint; Embedding, optimizer.py:86-97, is the state)."""
+        np.savez(path, y=self.y.cpu().numpy(), v=self.v.cpu().numpy(),
+                 g=self.g.cpu().numpy(), iteration=np.array(self.iteration),
+                 rng_seed=np.array(self.rng_seed))
+
+    @classmethod
+    def load(cls, path) -> "Embedding":
+        """Restore a checkpoint; an Engine built on it continues the schedule
+        at the saved iteration (exaggeration and momentum switches)."""
+        with np.load(path) as z:
+            e = embedding_from(z["y"], z["v"], z["g"],
+                               iteration=int(z["iteration"]))
+            e.rng_seed = int(z["rng_seed"])
+        return e
 
 
 @dataclass
@@ -747,6 +767,8 @@ class Engine:
                 for i in range(k):
                     for name, (a, b) in self._stage_events().items():
                         timings.add(name, evs[i][a].elapsed_time(evs[i][b]) * 1e-3)
+                    timings.add("iteration",
+                                evs[i][0].elapsed_time(evs[i][6]) * 1e-3)
                     if self.shard is not None:
                         timings.add("comm", (evs[i][4].elapsed_time(evs[i][5])
                                              + evs[i][8].elapsed_time(evs[i][6])) * 1e-3)

@@ -565,3 +565,23 @@ def test_sharded_engine_single_rank_matches_unsharded(bh):
     finally:
         dist.destroy_process_group()
     np.testing.assert_array_equal(e2.y.cpu().numpy(), e1.y.cpu().numpy())
+
+
+def test_checkpoint_resume_continues_the_schedule(bh, tmp_path):
+    """Embedding.save / load: 40 iterations, a checkpoint, 40 more from the
+    restored state (across the exaggeration switch at 50) equal 80 straight
+    iterations bit for bit (relabel off: both runs keep the id order)."""
+    a = golden("affinity450")
+    p = bh.from_csr(a["row_offsets"], a["col_indices"], a["values"])
+    cfg = bh.TsneConfig(n_iter=80, exaggeration_iters=50, graph_chunk=10,
+                        relabel_every=0)
+    e1 = bh.init_embedding(450, seed=5)
+    bh.Engine(p, e1, cfg).run(80)
+    e2 = bh.init_embedding(450, seed=5)
+    bh.Engine(p, e2, cfg).run(40)
+    e2.save(tmp_path / "ck.npz")
+    e3 = bh.Embedding.load(tmp_path / "ck.npz")
+    assert e3.iteration == 40
+    bh.Engine(p, e3, cfg).run(40)
+    np.testing.assert_array_equal(e3.y.cpu().numpy(), e1.y.cpu().numpy())
+    assert e3.iteration == 80
