@@ -216,11 +216,13 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle (reference restatement) timing
 # ---------------------------------------------------------------------------
-def cpu_oracle_time(prob, y, it0, steps, warmup=0, code_bits=32):
+def cpu_oracle_time(prob, y, it0, steps, warmup=0, code_bits=64):
     """Full oracle gradient iterations (the reference's algorithm restated in
     C/OpenMP, oracle/bh_oracle.c) on the host cores from state y at
     iteration it0, with the run() schedule's exaggeration (x12 below
-    iteration 250) and momentum; `warmup` untimed iterations first."""
+    iteration 250) and momentum; `warmup` untimed iterations first.
+    code_bits = 64: the reference's own Morton codes and depth-32 tree
+    (quadtree.py), as the reference runs."""
     from oracle import oracle as o
     threads = o.set_threads(0)
     n = int(prob["n"])
@@ -293,7 +295,8 @@ def reference_arm(args, rank, world):
                          "sample": f"{steps} full gradient iteration(s) of "
                                    f"{args.config} (iterations [{args.warmup}, "
                                    f"{args.warmup + steps}) of the schedule from "
-                                   f"Y0) on {threads} threads ({cpu_model()})"
+                                   f"Y0) on {threads} threads ({cpu_model()}), "
+                                   "the reference's 64-bit Morton codes"
                                    + (f"; requested {args.steps} steps capped at "
                                       f"{args.ref_max_steps}" if capped else ""),
                          "stage_s": stages},
@@ -653,7 +656,7 @@ def ours_arm(args, rank, world):
                "sample": f"{args.cpu_steps} full gradient iteration(s) of "
                          f"{args.config} (N={n}) from the Y after the timed "
                          f"region, C/OpenMP oracle on {threads} threads "
-                         f"({cpu_model()})",
+                         f"({cpu_model()}), the reference's 64-bit codes",
                "stage_s": stages}
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,

@@ -182,7 +182,6 @@ def cmd_run():
             wall_s=np.array(wall), knn_sha256=np.array(graph_sha(idx, sqd)),
             snap_iterations=np.array(SNAP),
             **{f"y{t}": snaps[t].astype(np.float32) for t in SNAP},
-            y_final=np.column_stack([e.y0, e.y1]).astype(np.float32),
             stage_s=np.array([timings.total(s) for s in
                               ("tree", "summarize", "attractive",
                                "repulsive", "update")]))
