@@ -59,14 +59,22 @@ k_tree_count(const K *__restrict__ sc, int64_t n,
     uint32_t cnt[D + 1];
 #pragma unroll
     for (int d = 0; d <= D; d++) cnt[d] = 0;
+    // all chunks' code loads in flight together (unrolled)
+    int lo_[kTreePPT], hi_[kTreePPT];
+#pragma unroll
     for (int j = 0; j < kTreePPT; j++) {
         int64_t t = (int64_t)blockIdx.x * kTreeChunk + j * kTreeThreads + threadIdx.x;
-        int lo = D + 1, hi = -1;
+        lo_[j] = D + 1;
+        hi_[j] = -1;
         if (t < n) {
             int s0 = same_digits(sc, t, n, D), s1 = same_digits(sc, t + 1, n, D);
-            lo = s0 + 1;
-            hi = min(D, 1 + max(s0, s1));
+            lo_[j] = s0 + 1;
+            hi_[j] = min(D, 1 + max(s0, s1));
         }
+    }
+#pragma unroll
+    for (int j = 0; j < kTreePPT; j++) {
+        const int lo = lo_[j], hi = hi_[j];
 #pragma unroll
         for (int d = 0; d <= D; d++)
             cnt[d] += __popc(__ballot_sync(0xffffffffu, lo <= d && d <= hi));
@@ -582,8 +590,16 @@ extern "C" int bh_summarize_prefix(const bh_tree_t *t, void *ws,
     cudaStream_t st = bh_cs(stream);
     BH_LAUNCH("k_prefix_scan", k_prefix_scan<float>, L.nblk, kPsThreads, 0,
               st, (const float2 *)t->ys, t->n_points, tsum, S, t->status);
-    int grid = bh_blocks(t->node_capacity, kSumThreads);
-    if (grid > kSumBlocks) grid = kSumBlocks;
+    // about one node per thread (a tree has at most ~n nodes in practice;
+    // the grid-stride loop covers any more): the gathers of a node are
+    // dependent, so memory-level parallelism comes from threads
+    static const int per_thread = [] {  // tuning knob BH_SUMP_NODES
+        const char *s = getenv("BH_SUMP_NODES");
+        const int v = s ? atoi(s) : 1;
+        return v > 0 ? v : 1;
+    }();
+    const int grid = (int)std::max<int64_t>(
+        1, bh_blocks(t->n_points, (int64_t)kSumThreads * per_thread));
     BH_LAUNCH("k_summarize_prefix", k_summarize_prefix<float>, grid,
               kSumThreads, 0, st, (void *)t->node, t->parent, t->node_start,
               t->leaf_end, (const float2 *)t->ys, (const double2 *)S,

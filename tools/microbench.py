@@ -111,6 +111,8 @@ def child(args):
     if args.precision == "f32":
         out["summarize_prefix_ms"] = timeit(lambda: t.summarize_prefix(),
                                             args.reps)
+        out["tree_build_prefix_ms"] = timeit(
+            lambda: (t.build(eng.y), t.summarize_prefix()), args.reps)
     print(json.dumps(out), flush=True)
 
 
