@@ -64,7 +64,8 @@ def child(args):
     eng.load()
     eng.begin()
     build()
-    eng.relabel()  # storage (Y and P) in Morton order, as in the engine
+    if not args.input_order:
+        eng.relabel()  # storage (Y and P) in tree order, as in the engine
     eng.begin()
     build()
     torch.cuda.synchronize()
@@ -123,6 +124,8 @@ def main():
     ap.add_argument("--theta", type=float, default=0.5)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--input-order", action="store_true",
+                    help="keep the input's storage order (a run's first 50 iterations)")
     ap.add_argument("--precision", choices=["f32", "f64"], default="f32")
     ap.add_argument("--sweep", nargs="*", default=[],
                     help="NAME=v1,v2,... environment knobs to sweep")
@@ -138,6 +141,8 @@ def main():
         cmd = [sys.executable, __file__, "--child", "--config", args.config,
                "--preroll", str(args.preroll), "--theta", str(args.theta),
                "--reps", str(args.reps), "--precision", args.precision]
+        if args.input_order:
+            cmd.append("--input-order")
         subprocess.run(cmd, env=env, check=False)
 
 

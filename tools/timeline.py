@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--theta", type=float, default=0.5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--input-order", action="store_true",
+                    help="keep the input's storage order (iterations < 50 of a run)")
     args = ap.parse_args()
 
     import numpy as np
@@ -51,9 +53,11 @@ def main():
         os.makedirs(os.path.dirname(cache), exist_ok=True)
         np.save(cache, e.y.cpu().numpy())
     eng = bh.Engine(p, e, cfg)
-    eng.initial_relabel = True  # storage order = the tree order of this Y
+    # storage order = the tree order of this Y (as after a relabel), or the
+    # input's own order (a run before its first relabel)
+    eng.initial_relabel = not args.input_order
     eng.prepare()
-    eng.run(20)  # warm: graphs captured, caches hot
+    eng.run(3 if args.input_order else 20)  # warm: graphs captured
     eng.relabel_every = 0  # a relabel inside the window would skew it
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
