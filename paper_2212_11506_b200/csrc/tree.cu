@@ -178,19 +178,20 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
         }
         __syncthreads();
         if (threadIdx.x <= D) {
+            // per warp: the level's id base of the warp's first lane
             uint32_t s = s_carry[threadIdx.x];
             for (int w = 0; w < kTreeWarps; w++) {
-                s_woff[w][threadIdx.x] = s;
+                s_woff[w][threadIdx.x] = (uint32_t)s_base[threadIdx.x] + s;
                 s += __popc(s_bal[w][threadIdx.x]);
             }
             s_carry[threadIdx.x] = s;
         }
         __syncthreads();
         if (t < n) {
-            // exclusive rank (global node-id base) of t on level d
+            // exclusive rank (global node-id base) of t on level d: the id
+            // of t's level-d node if t starts one, else that id + 1
             auto base = [&](int d) -> int32_t {
-                return s_base[d] + (int32_t)s_woff[warp][d] +
-                       __popc(s_bal[warp][d] & lt);
+                return (int32_t)s_woff[warp][d] + __popc(s_bal[warp][d] & lt);
             };
             const int32_t pid = order[t];
             const p2_t<T> p = y[pid];
@@ -198,26 +199,36 @@ k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
             sx = __dadd_rn(sx, (double)p.x);
             sy = __dadd_rn(sy, (double)p.y);
             if (rank) rank[pid] = (int32_t)t;
-            for (int d = lo; d <= hi; d++) {
-                const int32_t id = base(d);
-                const bool leaf = (s1 < d) || d == D;
-                parent[id] = d == 0 ? -1 : (d == lo ? base(d - 1) - 1 : base(d - 1));
-                node_start[id] = (int32_t)t;
-                if (!leaf) {
-                    Rec::store_info(node, id, (uint32_t)base(d + 1));
-                } else if (s1 < D) {
-                    // single-point leaf: complete record (quadtree.py:490-498)
-                    Rec::store(node, id, p, 1u, BH_LEAF_BIT | (uint32_t)t);
-                } else {
-                    // first point of a run of equal codes (depth-D bucket)
-                    Rec::store_info(node, id, BH_LEAF_BIT | (uint32_t)t);
+            // one pass over the levels t starts a node on or ends one on
+            // (each level's base evaluated once): t starts a node on
+            // d in [lo, hi] and is the last point of its node on d in
+            // [s1 + 1, hi] -- the node's end (leaf_end holds the end of
+            // every node, leaves and internal)
+            const int dend = max(s1 + 1, 0);
+            int d = min(lo, dend);
+            int32_t b = d <= hi ? base(d) : 0;
+            int32_t bprev = (d <= hi && d == lo && d > 0) ? base(d - 1) : 0;
+            for (; d <= hi; d++) {
+                const int32_t bnext = d < hi ? base(d + 1) : 0;
+                if (d >= lo) {
+                    const int32_t id = b;
+                    const bool leaf = (s1 < d) || d == D;
+                    parent[id] = d == 0 ? -1 : (d == lo ? bprev - 1 : bprev);
+                    node_start[id] = (int32_t)t;
+                    if (!leaf) {
+                        Rec::store_info(node, id, (uint32_t)bnext);
+                    } else if (s1 < D) {
+                        // single-point leaf: complete record (quadtree.py:490-498)
+                        Rec::store(node, id, p, 1u, BH_LEAF_BIT | (uint32_t)t);
+                    } else {
+                        // first point of a run of equal codes (depth-D bucket)
+                        Rec::store_info(node, id, BH_LEAF_BIT | (uint32_t)t);
+                    }
                 }
+                if (d >= dend) leaf_end[d >= lo ? b : b - 1] = (int32_t)(t + 1);
+                bprev = b;
+                b = bnext;
             }
-            // t is the last point of its level-d node for every level d
-            // deeper than the prefix it shares with t + 1: the node's end
-            // (leaf_end holds the end of every node, leaves and internal)
-            for (int d = max(s1 + 1, 0); d <= hi; d++)
-                leaf_end[d >= lo ? base(d) : base(d) - 1] = (int32_t)(t + 1);
         }
         __syncthreads();
     }
