@@ -358,6 +358,10 @@ class Engine:
         # iterations and the run starts in the input's own order)
         self.initial_relabel = os.environ.get("BH_INITIAL_RELABEL", "0") == "1"
         self.launches = 0  # library kernels enqueued by run() (bench claim)
+        # False once a capture failed: a sharded engine then enqueues its
+        # iterations eagerly (NCCL collectives inside CUDA graphs depend on
+        # the torch / NCCL build; the single-GPU path always captures)
+        self.graphs_ok = True
         # True: full chunks of the fast path replay one graph_chunk-iteration
         # graph (+0.2% device time, but capturing 25-iteration graphs for the
         # three CSR buffers costs ~0.1 s per engine: off for end-to-end runs)
@@ -554,6 +558,22 @@ class Engine:
         if name is not None:
             torch.cuda.nvtx.range_push(name)
 
+    def _capture_or_eager(self, make):
+        """make() -> graph; on a failed capture of a sharded engine, fall
+        back to eager iterations (returns None) instead of failing the run."""
+        try:
+            return make()
+        except Exception as exc:  # noqa: BLE001 - re-raised without a shard
+            if self.shard is None:
+                raise
+            import sys
+            print(f"[engine] CUDA graph capture with collectives failed "
+                  f"({type(exc).__name__}: {exc}); running eager iterations",
+                  file=sys.stderr)
+            self.graphs_ok = False
+            torch.cuda.synchronize()
+            return None
+
     def _capture(self, enqueue):
         """Capture `enqueue()` on the main stream into a CUDA graph.  The
         loop allocates nothing (every buffer is preallocated), so the capture
@@ -622,7 +642,8 @@ class Engine:
         with torch.cuda.stream(self.main):
             for key in keys:
                 self.csr_key = key
-                self._graph1()
+                if self._capture_or_eager(self._graph1) is None:
+                    break
                 if self.chunk_graph:
                     self._graphk()
                 if timings:
@@ -744,19 +765,24 @@ class Engine:
         while done < n_iter:
             k = min(chunk, n_iter - done)
             evs = None
-            if use_graph and timings is None:
+            g = None
+            if use_graph and self.graphs_ok and timings is None:
                 if self.chunk_graph and k == self.cfg.graph_chunk:
-                    self._graphk().replay()
+                    g = self._capture_or_eager(self._graphk)
+                    if g is not None:
+                        g.replay()
                 else:
-                    g = self._graph1()
-                    for _ in range(k):
+                    g = self._capture_or_eager(self._graph1)
+                    for _ in range(k if g is not None else 0):
                         torch.cuda.nvtx.range_push("iteration")
                         g.replay()
                         torch.cuda.nvtx.range_pop()
-            elif use_graph:
-                g, evs = self._graph(k)
-                g.replay()
-            else:
+            elif use_graph and self.graphs_ok:
+                ge = self._capture_or_eager(lambda: self._graph(k))
+                if ge is not None:
+                    g, evs = ge
+                    g.replay()
+            if g is None:  # eager (use_graph=False, or no capture possible)
                 evs = self._events(k) if timings is not None else None
                 for i in range(k):
                     self._enqueue(evs[i] if evs else None)

@@ -119,3 +119,27 @@ def test_device_partition_equals_host_mirror(bh, world):
         np.testing.assert_array_equal(pt[:, 1], host[1:])
         np.testing.assert_array_equal(
             pt[:, 2], host[:-1] + np.floor(0.35 * np.diff(host)).astype(np.int64))
+
+
+def test_nccl_collectives_in_graphs(bh):
+    """The product transport: a one-rank NCCL group (two ranks cannot share
+    a GPU), so the Z all-reduce and the Y all-gather run through
+    ProcessGroupNCCL and are captured in the iteration's CUDA graph; the
+    trajectory equals the unsharded engine's bitwise."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+               RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                         "nccl_world1_child.py")
+    r = subprocess.run([sys.executable, child], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out == {"graphs_ok": True, "equal": True, "finite": True}, (out, r.stderr[-2000:])
