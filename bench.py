@@ -58,6 +58,16 @@ def log(*a):
 # symmetrisation torch ops, Y0 numpy's Philox -- so the reference arm never
 # loads libbhtsne_b200.so)
 # ---------------------------------------------------------------------------
+# BH_BENCH_SHARD1=1: run a one-GPU bench through the multi-GPU code path
+# (a one-rank NCCL group, the sharded engine, its collectives captured in
+# the iteration graphs) -- the N>1 path exercised on a one-GPU box
+FORCE_SHARD = os.environ.get("BH_BENCH_SHARD1") == "1"
+
+
+def _dist(world):
+    return world > 1 or FORCE_SHARD
+
+
 def knn_torch(x: np.ndarray, k: int, dev):
     """kNN graph for the benchmark inputs (setup only): fp32 distances via
     cuBLAS, top-k per row; ascending, self excluded."""
@@ -479,7 +489,7 @@ def ours_arm(args, rank, world):
                         relabel_every=args.relabel_every)
     e = bh.embedding_from(prob["y0"])
     shard = None
-    if world > 1:
+    if _dist(world):
         from paper_2212_11506_b200.dist import Shard
         shard = Shard(rank, world)
     eng = bh.Engine(p, e, cfg, schedule=True, shard=shard)
@@ -493,7 +503,7 @@ def ours_arm(args, rank, world):
     eng.run(args.warmup)
     torch.cuda.synchronize()
     # --- timed region: K iterations, CUDA events on the launching stream
-    if world > 1:
+    if _dist(world):
         dist.barrier()
     torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
@@ -507,7 +517,7 @@ def ours_arm(args, rank, world):
     torch.cuda.synchronize()
     ms = start.elapsed_time(stop)
     launches = eng.launches - launches0
-    if world > 1:
+    if _dist(world):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -674,14 +684,14 @@ def ours_arm(args, rank, world):
 
 
 def _shard(rank, world):
-    if world == 1:
+    if not _dist(world):
         return None
     from paper_2212_11506_b200.dist import Shard
     return Shard(rank, world)
 
 
 def _max_over_ranks(seconds, world):
-    if world == 1:
+    if not _dist(world):
         return seconds
     import torch
     import torch.distributed as dist
@@ -851,7 +861,7 @@ def c4_arm(args, rank, world):
     def timed(fn, reps):
         fn()
         torch.cuda.synchronize()
-        if world > 1:
+        if _dist(world):
             dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -861,7 +871,7 @@ def c4_arm(args, rank, world):
         b.record()
         b.synchronize()
         ms = a.elapsed_time(b) / reps
-        if world > 1:
+        if _dist(world):
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
@@ -964,9 +974,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    if world > 1:
+    if _dist(world):
         import torch
         import torch.distributed as dist
+        if world == 1:  # BH_BENCH_SHARD1 without torchrun
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
     try:
@@ -983,7 +998,7 @@ def main():
         else:
             ours_arm(args, rank, world)
     finally:
-        if world > 1:
+        if _dist(world):
             import torch.distributed as dist
             dist.barrier()
             dist.destroy_process_group()
