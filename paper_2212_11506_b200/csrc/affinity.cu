@@ -441,6 +441,10 @@ struct PermLen {
     }
 };
 
+// 8 lanes per row, 4 rows per warp in flight: rows whose source and
+// destination start on a 4-entry boundary and whose length is a multiple
+// of 4 (every row of the engine's padded CSR) move as 16-B column / value
+// vectors, 4 independent rank gathers per lane; other rows entry by entry.
 template <typename V>
 __global__ void k_permute_csr_fill(const int64_t *__restrict__ rp,
                                    const int32_t *__restrict__ col,
@@ -450,14 +454,25 @@ __global__ void k_permute_csr_fill(const int64_t *__restrict__ rp,
                                    const int64_t *__restrict__ orp,
                                    int32_t *__restrict__ ocol,
                                    V *__restrict__ oval) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = wid; r < n; r += nw) {
+    constexpr int L = 8;  // lanes per row
+    const int gl = threadIdx.x & (L - 1);
+    const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / L;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / L;
+    for (int64_t r = grp; r < n; r += ng) {
         const int64_t o = perm[r], s = rp[o], len = rp[o + 1] - s, d = orp[r];
-        for (int64_t q = lane; q < len; q += 32) {
-            ocol[d + q] = rank[col[s + q]];
-            oval[d + q] = val[s + q];
+        if (sizeof(V) == 4 && ((s | d | len) & 3) == 0) {
+            for (int64_t q = 4 * gl; q < len; q += 4 * L) {
+                const int4 c = *(const int4 *)(col + s + q);
+                const float4 v = *(const float4 *)((const float *)val + s + q);
+                *(int4 *)(ocol + d + q) =
+                    make_int4(rank[c.x], rank[c.y], rank[c.z], rank[c.w]);
+                *(float4 *)((float *)oval + d + q) = v;
+            }
+        } else {
+            for (int64_t q = gl; q < len; q += L) {
+                ocol[d + q] = rank[col[s + q]];
+                oval[d + q] = val[s + q];
+            }
         }
     }
 }
@@ -487,8 +502,8 @@ static int permute_impl(const int64_t *row_ptr, const int32_t *col,
                                   ws, st);
     if (rc != BH_OK) return rc;
     k_set_last<<<1, 1, 0, st>>>(out_row_ptr, n, total);
-    int grid = bh_blocks(n, 8);
-    if (grid > kSMs * 32) grid = kSMs * 32;
+    int grid = bh_blocks(n, 256 / 8);
+    if (grid > kSMs * 16) grid = kSMs * 16;
     k_permute_csr_fill<V><<<grid, 256, 0, st>>>(row_ptr, col, val, perm, rank,
                                                 n, out_row_ptr, out_col, out_val);
     BH_CHECK_LAUNCH("k_permute_csr_fill");

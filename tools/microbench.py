@@ -109,6 +109,7 @@ def child(args):
                ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st),
                args.reps),
            "summarize_ms": timeit(lambda: t.summarize(), args.reps)}
+    out["relabel_ms"] = timeit(eng.relabel, max(2, args.reps // 4))
     if args.precision == "f32":
         out["summarize_prefix_ms"] = timeit(lambda: t.summarize_prefix(),
                                             args.reps)
