@@ -13,8 +13,9 @@
 // level_off[d] + (number of points before t that start a level-d node), so
 // the whole topology is one prefix count over the sorted codes:
 //   k_tree_count  per-CTA level histograms (warp ballots)
-//   k_tree_scan   one CTA: per-level scans -> CTA offsets, level_off, M
-//   k_tree_emit   per point: node ids by ballot-popc ranks, parents, and the
+//   k_tree_emit   per CTA: its level offsets from the counts of the lower
+//                 CTAs and the level totals (level_off, M, capacity check);
+//                 per point: node ids by ballot-popc ranks, parents, and the
 //                 complete record of every single-point leaf (its centre of
 //                 mass is the point itself: f64 sum of one value / 1)
 // Summarize then runs level by level, deepest first (the reference's own
@@ -91,76 +92,73 @@ k_tree_count(const K *__restrict__ sc, int64_t n,
     }
 }
 
-// One CTA of 1024 threads: warp w scans level w's CTA counts.
-template <int D>
-__global__ void __launch_bounds__(1024)
-k_tree_scan(const uint32_t *__restrict__ blk_counts, int nblk,
-            uint32_t *__restrict__ blk_off, int32_t *__restrict__ level_off,
-            int64_t capacity, int32_t *__restrict__ status) {
-    bh_pdl_trigger();  // the successor may launch early (PDL)
-    bh_pdl_wait();     // the predecessor's results are visible
-
-    __shared__ uint32_t s_tot[D + 1];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int d = warp; d <= D; d += 32) {
-        uint32_t carry = 0;
-        for (int b0 = 0; b0 < nblk; b0 += 32) {
-            int b = b0 + lane;
-            uint32_t v = b < nblk ? blk_counts[(size_t)b * (D + 1) + d] : 0u;
-            uint32_t x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (b < nblk) blk_off[(size_t)b * (D + 1) + d] = carry + x - v;
-            carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (lane == 0) s_tot[d] = carry;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        int levels = 0;
-        level_off[0] = 0;
-        for (int d = 0; d <= D; d++) {
-            acc += s_tot[d];
-            if (s_tot[d]) levels = d + 1;
-            level_off[d + 1] = (int32_t)(acc < 0x7fffffff ? acc : 0x7fffffff);
-        }
-        level_off[D + 2] = levels;
-        *status = (acc > capacity || acc >= (int64_t)BH_CHILD_MASK) ? BH_ERR_CAPACITY
-                                                                    : BH_OK;
-    }
-}
-
 template <typename K, int D, typename T>
 __global__ void __launch_bounds__(kTreeThreads)
 k_tree_emit(const K *__restrict__ sc, const int32_t *__restrict__ order,
             const p2_t<T> *__restrict__ y, int64_t n,
-            const uint32_t *__restrict__ blk_off,
-            const int32_t *__restrict__ level_off, void *__restrict__ node,
+            const uint32_t *__restrict__ blk_counts, int64_t capacity,
+            int32_t *__restrict__ level_off, void *__restrict__ node,
             int32_t *__restrict__ parent, int32_t *__restrict__ node_start,
             int32_t *__restrict__ leaf_end, p2_t<T> *__restrict__ ys,
             int32_t *__restrict__ rank, double2 *__restrict__ tile_sum,
-            const int32_t *__restrict__ status) {
+            int32_t *__restrict__ status) {
     bh_pdl_trigger();  // the successor may launch early (PDL)
     bh_pdl_wait();     // the predecessor's results are visible
 
     using Rec = NodeRec<T>;
-    if (*status != BH_OK) return;
     __shared__ double2 s_tsum[kTreeWarps];
     double sx = 0.0, sy = 0.0;  // this thread's points, in order (f64)
     __shared__ uint32_t s_bal[kTreeWarps][D + 1];
     __shared__ uint32_t s_woff[kTreeWarps][D + 1];
     __shared__ uint32_t s_carry[D + 1];
     __shared__ int32_t s_base[D + 1];
+    __shared__ uint32_t s_pre[D + 1], s_tot[D + 1];
+    __shared__ bool s_ok;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // The CTA's node-id offsets (no separate scan launch): per level, the
+    // nodes started in the lower blocks (k_tree_count's counts) and in all
+    // blocks -- integer sums, any order; level offsets from the totals.
     if (threadIdx.x <= D) {
         s_carry[threadIdx.x] = 0;
-        s_base[threadIdx.x] = level_off[threadIdx.x] +
-                              (int32_t)blk_off[(size_t)blockIdx.x * (D + 1) + threadIdx.x];
+        s_pre[threadIdx.x] = 0;
+        s_tot[threadIdx.x] = 0;
     }
+    __syncthreads();
+    for (int d = 0; d <= D; d++) {
+        uint32_t pre = 0, tot = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kTreeThreads) {
+            const uint32_t c = blk_counts[(size_t)b * (D + 1) + d];
+            tot += c;
+            pre += b < (int)blockIdx.x ? c : 0u;
+        }
+        pre = __reduce_add_sync(0xffffffffu, pre);
+        tot = __reduce_add_sync(0xffffffffu, tot);
+        if (lane == 0 && tot) {
+            atomicAdd(&s_tot[d], tot);
+            if (pre) atomicAdd(&s_pre[d], pre);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        int levels = 0;
+        for (int d = 0; d <= D; d++) {
+            s_base[d] = (int32_t)(acc < 0x7fffffff ? acc : 0x7fffffff);
+            acc += s_tot[d];
+            if (s_tot[d]) levels = d + 1;
+        }
+        const bool ok = acc <= capacity && acc < (int64_t)BH_CHILD_MASK;
+        s_ok = ok;
+        if (blockIdx.x == 0) {
+            for (int d = 0; d <= D; d++) level_off[d] = s_base[d];
+            level_off[D + 1] = (int32_t)(acc < 0x7fffffff ? acc : 0x7fffffff);
+            level_off[D + 2] = levels;
+            *status = ok ? BH_OK : BH_ERR_CAPACITY;
+        }
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    if (threadIdx.x <= D) s_base[threadIdx.x] += (int32_t)s_pre[threadIdx.x];
     const unsigned lt = lanemask_lt();
     for (int j = 0; j < kTreePPT; j++) {
         int64_t t = (int64_t)blockIdx.x * kTreeChunk + j * kTreeThreads + threadIdx.x;
@@ -498,14 +496,13 @@ static int build_impl(const bh_tree_t *t, const void *y, void *ws,
                       cudaStream_t st) {
     TreeLayout L = tree_layout(t->n_points, D);
     char *w = (char *)ws;
-    uint32_t *cnt = (uint32_t *)(w + L.counts), *off = (uint32_t *)(w + L.offs);
+    uint32_t *cnt = (uint32_t *)(w + L.counts);
     const K *sc = (const K *)t->sorted_codes;
     BH_LAUNCH("k_tree_count", (k_tree_count<K, D>), L.nblk, kTreeThreads, 0,
               st, sc, t->n_points, cnt);
-    BH_LAUNCH("k_tree_scan", k_tree_scan<D>, 1, 1024, 0, st, cnt, L.nblk, off, t->level_off,
-                                       t->node_capacity, t->status);
     BH_LAUNCH("k_tree_emit", (k_tree_emit<K, D, T>), L.nblk, kTreeThreads, 0, st,
-        sc, t->order, (const p2_t<T> *)y, t->n_points, off, t->level_off,
+        sc, t->order, (const p2_t<T> *)y, t->n_points, cnt, t->node_capacity,
+        t->level_off,
         (void *)t->node, t->parent, t->node_start, t->leaf_end,
         (p2_t<T> *)t->ys, t->rank, (double2 *)(w + L.tsum), t->status);
     return BH_OK;

@@ -224,7 +224,7 @@ def embedding_from(y, v=None, g=None, iteration=0, dtype=None) -> Embedding:
 
 # ---------------------------------------------------------------------------
 # Engine: every buffer of the loop preallocated in HBM; one iteration = one
-# Morton pass, the radix-sort passes, 3 tree kernels, the summarize kernels,
+# Morton pass, the radix-sort passes, 2 tree kernels, the summarize kernels,
 # the force pass (the side-stream CSR sweep + one fused launch), the update,
 # enqueued on the current stream and captured in CUDA graphs.  The state is
 # kept in a private "storage order", renumbered to the current Morton order
@@ -436,7 +436,7 @@ class Engine:
 
     def kernels_per_iteration(self, timed: bool = False) -> int:
         """Library kernel launches of one iteration: morton, sort histogram +
-        one pass per code byte, 3 tree kernels, the summarize kernels (2 for
+        one pass per code byte, 2 tree kernels, the summarize kernels (2 for
         the prefix summarize; else one per level below the top 7 plus one
         for levels 6..0, tree.cu), the side sweep, the force pass (1 fused
         or 2), update; + Z sum, unpack and finish when sharded."""
@@ -445,7 +445,7 @@ class Engine:
         top = min(int(os.environ.get("BH_SUM_TOP", 6)), depth)  # tree.cu
         summarize = (2 if self.prefix_summary
                      else depth - top + (1 if top >= 0 else 0))
-        return (1 + 1 + self.code_bits // 8 + 3 + summarize
+        return (1 + 1 + self.code_bits // 8 + 2 + summarize
                 + (1 if self._split_on() else 0) + forces + 1 + 1
                 + (6 if self.shard is not None else 0))
 
