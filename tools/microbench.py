@@ -109,6 +109,20 @@ def child(args):
                ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st),
                args.reps),
            "summarize_ms": timeit(lambda: t.summarize(), args.reps)}
+    # yardstick: cuSPARSE SpMM (torch CSR @ dense) of the same relabelled P
+    # with Y as the (N, 2) dense operand -- the sweep's gathers with
+    # plain multiply-adds (library code, not the product path)
+    try:
+        pc = torch.sparse_csr_tensor(eng.rp.int(), eng.col, eng.val,
+                                     size=(eng.n, eng.n))
+        yy = eng.y.view(eng.n, 2).contiguous()
+        out["cusparse_spmm_ms"] = timeit(lambda: torch.sparse.mm(pc, yy),
+                                         args.reps)
+        yx0, yx1 = yy[:, 0].contiguous(), yy[:, 1].contiguous()
+        out["cusparse_2spmv_ms"] = timeit(
+            lambda: (torch.mv(pc, yx0), torch.mv(pc, yx1)), args.reps)
+    except Exception as exc:  # noqa: BLE001 - yardstick only
+        out["cusparse_spmm_error"] = str(exc)[:200]
     out["relabel_ms"] = timeit(eng.relabel, max(2, args.reps // 4))
     if args.precision == "f32":
         out["summarize_prefix_ms"] = timeit(lambda: t.summarize_prefix(),
