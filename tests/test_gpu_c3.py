@@ -114,6 +114,74 @@ def test_c3_gradient_on_reference_trajectory(bh, oracle, c3p, ref, it):
     assert rel <= 1e-4, rel
 
 
+@pytest.mark.parametrize("it", [250, 500, 999])
+def test_c3_engine_gradient_on_reference_trajectory(bh, oracle, c3p, ref, it):
+    """The timed path itself -- the engine's Hilbert-ordered tree, prefix
+    summarize, fused force launch with the side-stream sweep and the Z block
+    sums -- at the reference trajectory's Y: the gradient it forms
+    (4 (attr - rep / Z), before its update) within 1e-4 of the oracle."""
+    _, p = c3p
+    y = ref[f"y{it}"]
+    pe = bh.set_exaggeration(p, 12.0 if it < 250 else 1.0)
+    ro, co, va = pe.to_reference()
+    g0, g1, _, _, z = oracle.gradient(y, ro, co, va, 0.5, code_bits=32)
+    want = np.column_stack([g0, g1]).astype(np.float64)
+    e = bh.embedding_from(y)
+    cfg = bh.TsneConfig(n_iter=1000, relabel_every=0)
+    eng = bh.Engine(p, e, cfg)
+    eng.set_iteration(it)
+    eng.run(1)  # storage order = point order (no relabel)
+    torch.cuda.synchronize()
+    assert eng.z == pytest.approx(z, rel=1e-6)
+    zf = np.float32(eng.z)
+    got = 4.0 * (eng.attr.cpu().numpy().astype(np.float64)
+                 - eng.rep.cpu().numpy().astype(np.float64) / zf)
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"\n[c3] engine, iteration {it}: gradient rel-L2 {rel:.2e}")
+    assert rel <= 1e-4, rel
+
+
+@pytest.mark.parametrize("it", [250, 999])
+def test_c3_prefix_summarize_on_reference_trajectory(bh, ref, it):
+    """The engine's f32 summarize (f64 prefix sums) against the bit-exact
+    one on the reference trajectory's Y: counts, child words and leaves
+    bitwise; internal centres within one f32 spacing of the exact mean
+    (exact integer prefix sums of the f32 points as the truth), or within
+    the f64 prefix sums' resolution, 4 eps64 max|S| / count: the prefix of
+    1.3M points in tree order reaches |S| ~ 5e6, so centres within ~1e-3
+    of the origin can be a few f32 spacings off (the reference's own
+    child-order f32 centres miss the exact mean by more spacings on more
+    nodes: 53 / 165 vs 8 / 42 at iteration 999)."""
+    y = ref[f"y{it}"]
+    c, r = bh.compute_bounds(y)
+    t = bh.summarize(bh.build_tree(bh.morton_codes(y, c, r), y))
+    a = t.arrays
+    m = int(a.level_off[a.max_depth + 1].item())
+    exact = a.node[:m].cpu().numpy().copy()
+    a.summarize_prefix()
+    torch.cuda.synchronize()
+    pref = a.node[:m].cpu().numpy()
+    np.testing.assert_array_equal(pref[:, 2:].view(np.uint32),
+                                  exact[:, 2:].view(np.uint32))
+    leaf = (exact[:, 3].view(np.uint32) & np.uint32(0x80000000)) != 0
+    np.testing.assert_array_equal(pref[leaf, :2].view(np.uint32),
+                                  exact[leaf, :2].view(np.uint32))
+    E = 160
+    ys = a.ys.cpu().numpy().astype(np.float64)
+    start = a.node_start[:m].cpu().numpy().astype(np.int64)[~leaf]
+    end = a.leaf_end[:m].cpu().numpy().astype(np.int64)[~leaf]
+    got = pref[~leaf, :2].astype(np.float64)
+    for ax in (0, 1):
+        q = np.concatenate([[0], np.cumsum(np.array(
+            [int(v) for v in ys[:, ax] * 2.0 ** E], dtype=object))])
+        true = np.array([float(v) for v in (q[end] - q[start])]) / 2.0 ** E / (end - start)
+        ulp = np.spacing(np.maximum(np.abs(true), np.abs(got[:, ax])).astype(np.float32))
+        smax = np.abs(np.cumsum(ys[:, ax])).max()
+        tol = np.maximum(ulp, 4 * np.finfo(np.float64).eps * smax / (end - start))
+        d = np.abs(got[:, ax] - true)
+        assert (d <= tol).all(), (ax, d.max())
+
+
 def test_c3_full_run_final_kl_within_1pct(bh, c3, ref):
     x, g = c3
     e, timings, kl = bh.run(x, bh.TsneConfig(kl_every=250), knn=g)
