@@ -56,10 +56,23 @@ def stand_in_shard(rank, world):
     from paper_2212_11506_b200.dist import Shard
 
     class StandInShard(Shard):
-        def _gather_rows(self, eng, dst):
+        prefilled = False  # set once gbuf holds every share of the state
+
+        def prefill(self, eng, src):
             for r in range(self.world):
-                call("bh_pack_rows", ptr(dst), ptr(eng.parts[r]), eng.cap,
+                call("bh_pack_rows", ptr(src), ptr(eng.parts[r]), eng.cap,
                      eng.pt_bytes, ptr(self.gbuf[r * eng.cap:]), stream())
+            self.prefilled = True
+
+        def _gather_rows(self, eng, dst):
+            # before the timed graph: keep every share real by packing them
+            # all; the timed iteration (its state restored before each
+            # replay) leaves the other shares' gathered rows as prefilled,
+            # so only this rank's own work is timed
+            if not self.prefilled:
+                for r in range(self.world):
+                    call("bh_pack_rows", ptr(dst), ptr(eng.parts[r]), eng.cap,
+                         eng.pt_bytes, ptr(self.gbuf[r * eng.cap:]), stream())
             super()._gather_rows(eng, dst)
 
     return StandInShard(rank, world, comm=StandInComm(rank))
@@ -74,6 +87,10 @@ def time_iteration(eng, reps):
             dst.copy_(src)
 
     times = []
+    if eng.shard is not None:
+        eng.shard.prefill(eng, eng.y)
+        torch.cuda.synchronize()
+    eng.graphs.clear()  # captured after the prefill
     graph = eng._graph1()  # the fast path's one-iteration graph
     with torch.cuda.stream(eng.main):
         for _ in range(reps + 2):
@@ -87,7 +104,18 @@ def time_iteration(eng, reps):
             times.append(a.elapsed_time(b))
         restore()
     times = sorted(times[2:])
-    return times[len(times) // 2]
+    # one evented replay (the timed-stage graph) for the per-stage split
+    eng.fuse_timed = True
+    g, evs = eng._graph(1)
+    with torch.cuda.stream(eng.main):
+        restore()
+        g.replay()
+        torch.cuda.synchronize()
+        stages = {name: evs[0][a].elapsed_time(evs[0][b])
+                  for name, (a, b) in eng._stage_events().items()}
+        stages["iteration"] = evs[0][0].elapsed_time(evs[0][6])
+        restore()
+    return times[len(times) // 2], stages
 
 
 def main():
@@ -118,7 +146,7 @@ def main():
                        "the buffer at bw, plus lat_us each"}}
     base = None
     for world in (1, 2, 4, 8):
-        worst, per_rank = 0.0, []
+        worst, per_rank, stage_rows = 0.0, [], []
         for r in range(world):
             e2 = bh.Embedding(y=e.y.clone(), v=e.v.clone(), g=e.g.clone(),
                               iteration=e.iteration)
@@ -128,8 +156,9 @@ def main():
             eng.relabel()        # storage = tree order, shares re-balanced
             eng.begin()          # bounds of the centred Y, no pending shift
             torch.cuda.synchronize()
-            ms = time_iteration(eng, args.reps)
+            ms, stages = time_iteration(eng, args.reps)
             per_rank.append(ms)
+            stage_rows.append({k: round(v, 4) for k, v in stages.items()})
             worst = max(worst, ms)
             del eng
             torch.cuda.empty_cache()
@@ -142,6 +171,7 @@ def main():
         if base is None:
             base = step
         out[f"G{world}"] = {"per_rank_ms": per_rank, "max_rank_ms": worst,
+                            "stages_ms_rank0": stage_rows[0],
                             "comm_model_ms": comm_ms, "step_ms": step,
                             "projected_it_s": 1e3 / step,
                             "speedup_vs_1": base / step}
