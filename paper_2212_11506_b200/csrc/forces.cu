@@ -27,11 +27,16 @@ namespace bh {
 // ---------------------------------------------------------------------------
 // Per-pop context of a lane: its point, the group's R2 and whether the lane
 // opened the node whose children are being visited.
+#ifndef BH_R2_MASK
+#define BH_R2_MASK 1
+#endif
+
 struct GroupCtx {
     const float4 *__restrict__ node;
     const float2 *__restrict__ ys;
     float2 yi;
-    float r2;
+    float r2;   // this lane's acceptance threshold (R2, or -1: not in the mask)
+    float r2u;  // the group's R2 (pushed, quartered, with its children)
     bool mine;
     uint32_t self;
     int lane;
@@ -109,7 +114,13 @@ __device__ __forceinline__ uint32_t bh_child_fast(const GroupCtx &g,
     // z and 0 to the force, and rep_block subtracts that 1 (kScTheta)
     const bool use = acc && (SC || info != (BH_LEAF_BIT | g.self));
     const float w = use ? r.z : 0.f;  // the cell's point count
+#if BH_R2_MASK
+    // lanes outside the mask carry R2 = -1: they accept every child, so
+    // they never ask for children (their sums are zeroed per group)
+    const uint32_t need = ballot_full(!acc);
+#else
     const uint32_t need = ballot_full(g.mine && !acc);
+#endif
     const float k = rcp_approx(1.0f + d2);
     const float wk = w * k, wk2 = wk * k;
     if (FIRST) {  // the group's first term starts the partials (no 0 + x)
@@ -161,7 +172,7 @@ __device__ __forceinline__ void bh_group(const GroupCtx &g, uint32_t first,
     const uint32_t nz = ballot_full(push);
     if (push)
         stk[sp + __popc(nz >> (g.lane + 1))] = make_uint4(
-            info, msk, __float_as_uint(g.r2 * 0.25f), g.depth + 1u);
+            info, msk, __float_as_uint(g.r2u * 0.25f), g.depth + 1u);
     sp += __popc(nz);
 }
 
@@ -322,8 +333,13 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         const uint32_t first = ent.x & BH_CHILD_MASK;
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const bool mine = (ent.y >> lane) & 1u;
-        const float r2 = __uint_as_float(ent.z);
-        const GroupCtx g{node, ys, yi, r2, mine, self, lane, ent.w};
+        const float r2u = __uint_as_float(ent.z);
+#if BH_R2_MASK
+        const float r2 = mine ? r2u : -1.0f;
+#else
+        const float r2 = r2u;
+#endif
+        const GroupCtx g{node, ys, yi, r2, r2u, mine, self, lane, ent.w};
         // straight-line code for the (warp-uniform) number of children;
         // the branch-free body above the deepest level (warp-uniform)
         if (ent.w < (uint32_t)D) {
