@@ -453,15 +453,6 @@ __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
         yi = y[row];
     }
     double a0 = 0.0, a1 = 0.0;
-    if (PADDED) {
-        for (int64_t q = s + 4 * gl; q < e; q += 4 * G) {
-            // the CSR stream bypasses L1 (no allocation) so that L1 holds the
-            // y_j gathers
-            const int4 c = ld_stream_i4(col + q);
-            const float4 v = ld_stream_f4(val + q);
-            const float2 y0 = __ldg(&y[c.x]), y1 = __ldg(&y[c.y]);
-            const float2 y2 = __ldg(&y[c.z]), y3 = __ldg(&y[c.w]);
-            float fx = 0.f, fy = 0.f;
 #define BH_ATTR_TERM(YJ, V)                                                   \
     {                                                                         \
         float dx = yi.x - YJ.x, dy = yi.y - YJ.y;                             \
@@ -469,6 +460,21 @@ __device__ __forceinline__ void att_block(const AttArgs &A, int64_t bid,
         fx += pq * dx;                                                        \
         fy += pq * dy;                                                        \
     }
+    if (PADDED) {
+        // 32-bit offsets from the row start: fewer loop instructions than
+        // 64-bit indices (a second loop body without the exaggeration
+        // multiply made the fused kernel slower: code size)
+        const int32_t *__restrict__ cp = col + s;
+        const float *__restrict__ vp = val + s;
+        const int len = (int)(e - s);
+        for (int k = 4 * gl; k < len; k += 4 * G) {
+            // the CSR stream bypasses L1 (no allocation) so that L1 holds the
+            // y_j gathers
+            const int4 c = ld_stream_i4(cp + k);
+            const float4 v = ld_stream_f4(vp + k);
+            const float2 y0 = __ldg(&y[c.x]), y1 = __ldg(&y[c.y]);
+            const float2 y2 = __ldg(&y[c.z]), y3 = __ldg(&y[c.w]);
+            float fx = 0.f, fy = 0.f;
             BH_ATTR_TERM(y0, v.x)
             BH_ATTR_TERM(y1, v.y)
             BH_ATTR_TERM(y2, v.z)
