@@ -81,7 +81,9 @@ __device__ __forceinline__ uint32_t bh_child64(const Ctx64 &g, double2 c,
         a.r0 = __dadd_rn(a.r0, __dmul_rn(mk2, dx));
         a.r1 = __dadd_rn(a.r1, __dmul_rn(mk2, dy));
     }
-    return ballot_full(g.mine && !acc);
+    // lanes outside the mask carry side2 = -1 (Ctx64): they accept every
+    // cell, so the ballot of the lanes that open it needs no mask term
+    return ballot_full(!acc);
 }
 
 // The CNT children of one popped group, in order (the reference's
@@ -190,8 +192,9 @@ __device__ __forceinline__ void rep_block64(const RepArgs64 &A, int64_t bid,
         const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const double side2 = __longlong_as_double(
             (long long)(((unsigned long long)ent.w << 32) | ent.z));
-        const Ctx64 g{A.node, A.ys, yi, side2, theta2, ((ent.y >> lane) & 1u) != 0,
-                      self, lane};
+        const bool mine = ((ent.y >> lane) & 1u) != 0;
+        const Ctx64 g{A.node, A.ys, yi, mine ? side2 : -1.0, theta2, mine, self,
+                      lane};
         uint32_t info = 0, msk = 0;
         // straight-line code per (warp-uniform) child count, every record of
         // the group loaded up front; full groups tested first on the raw word
