@@ -64,7 +64,12 @@ def child(args):
     eng.load()
     eng.begin()
     build()
-    if not args.input_order:
+    if args.shuffle:
+        # a random storage order (an input given in arbitrary order)
+        g = torch.Generator(device="cpu").manual_seed(7)
+        t.order.copy_(torch.randperm(eng.n, generator=g).to(torch.int32))
+        eng.relabel()
+    elif not args.input_order:
         eng.relabel()  # storage (Y and P) in tree order, as in the engine
     eng.begin()
     build()
@@ -141,6 +146,8 @@ def main():
     ap.add_argument("--child", action="store_true")
     ap.add_argument("--input-order", action="store_true",
                     help="keep the input's storage order (a run's first 50 iterations)")
+    ap.add_argument("--shuffle", action="store_true",
+                    help="a random storage order (inputs in arbitrary order)")
     ap.add_argument("--precision", choices=["f32", "f64"], default="f32")
     ap.add_argument("--sweep", nargs="*", default=[],
                     help="NAME=v1,v2,... environment knobs to sweep")
@@ -158,6 +165,8 @@ def main():
                "--reps", str(args.reps), "--precision", args.precision]
         if args.input_order:
             cmd.append("--input-order")
+        if args.shuffle:
+            cmd.append("--shuffle")
         subprocess.run(cmd, env=env, check=False)
 
 
