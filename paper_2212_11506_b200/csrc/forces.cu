@@ -331,7 +331,6 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
         BH_DASSERT(sp >= 1 && sp <= CAP);
         const uint4 ent = stk[--sp];
         const uint32_t first = ent.x & BH_CHILD_MASK;
-        const int cnt = (int)(ent.x >> BH_NKIDS_SHIFT) + 1;
         const bool mine = (ent.y >> lane) & 1u;
         const float r2u = __uint_as_float(ent.z);
 #if BH_R2_MASK
@@ -346,11 +345,13 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
             // most groups are full (4 children): test that first, on the
             // raw word (info bits 29-30 = 3; a compare the compiler does
             // not fold into a jump table with the other counts)
+            // (the child count sits in bits 29-30 of the word, above the
+            // first child's index: the compares need no shift)
             if (__builtin_expect(ent.x >= (3u << BH_NKIDS_SHIFT), 1))
                 bh_group<4, COUNT, SC>(g, first, a, cn, stk, sp);
-            else if (cnt == 3)
+            else if (ent.x >= (2u << BH_NKIDS_SHIFT))
                 bh_group<3, COUNT, SC>(g, first, a, cn, stk, sp);
-            else if (cnt == 2)
+            else if (ent.x >= (1u << BH_NKIDS_SHIFT))
                 bh_group<2, COUNT, SC>(g, first, a, cn, stk, sp);
             else
                 bh_group<1, COUNT, SC>(g, first, a, cn, stk, sp);
@@ -358,9 +359,9 @@ __device__ __forceinline__ void rep_block(const RepArgs &A, int64_t bid,
             // children at depth D: all leaves, nothing to push
             if (ent.x >= (3u << BH_NKIDS_SHIFT))
                 bh_group_leaves<4, COUNT, SC>(g, first, a, cn);
-            else if (cnt == 3)
+            else if (ent.x >= (2u << BH_NKIDS_SHIFT))
                 bh_group_leaves<3, COUNT, SC>(g, first, a, cn);
-            else if (cnt == 2)
+            else if (ent.x >= (1u << BH_NKIDS_SHIFT))
                 bh_group_leaves<2, COUNT, SC>(g, first, a, cn);
             else
                 bh_group_leaves<1, COUNT, SC>(g, first, a, cn);
