@@ -354,7 +354,9 @@ NCU_METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,"
                "dram__bytes_write.sum,smsp__inst_executed.sum,"
                "smsp__issue_active.avg.pct_of_peak_sustained_active,"
                "l1tex__t_sector_hit_rate.pct,lts__t_sector_hit_rate.pct,"
-               "l1tex__throughput.avg.pct_of_peak_sustained_active")
+               "l1tex__throughput.avg.pct_of_peak_sustained_active,"
+               "l1tex__data_pipe_lsu_wavefronts.sum,"
+               "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")
 
 
 def ncu_child(args):
@@ -631,7 +633,9 @@ def ours_arm(args, rank, world):
                     "l1_hit_pct": row.get("l1tex__t_sector_hit_rate.pct"),
                     "l2_hit_pct": row.get("lts__t_sector_hit_rate.pct"),
                     "l1tex_throughput_pct": row.get(
-                        "l1tex__throughput.avg.pct_of_peak_sustained_active")}
+                        "l1tex__throughput.avg.pct_of_peak_sustained_active,"
+               "l1tex__data_pipe_lsu_wavefronts.sum,"
+               "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")}
     kd = kernels[dom]
     roof = {"bound": "hbm", "kernel": dom,
             "achieved": kd["achieved_gbs"], "peak": peak, "unit": "GB/s",
@@ -648,6 +652,18 @@ def ours_arm(args, rank, world):
                        "y_j gathers (sweep CTAs); see kernels.*.ncu",
             "visits_per_point": (cnt[0] + cnt[1]) / n,
             "leaf_points_per_point": cnt[2] / n}
+    # each kernel against the resource that binds it (ncu, same launch):
+    # the sweep's L1 data-pipe wavefronts, the traversal's issue slots
+    binding = {}
+    for name, res, key in (("attractive", "L1 data-pipe wavefronts",
+                            "l1_wavefront_pct"),
+                           ("repulsive", "issue slots", "issue_active_pct"),
+                           ("forces", "issue slots", "issue_active_pct")):
+        kn = kernels.get(name, {}).get("ncu")
+        if kn and kn.get(key) is not None:
+            binding[name] = {"resource": res, "frac": kn[key] / 100.0}
+    if binding:
+        roof["binding_roofline"] = binding
 
     # --- e2e through the public API with host buffers
     vals = sorted(r["value"] for r in runs)

@@ -98,6 +98,14 @@ def child(args):
                          ptr(eng.col), ptr(eng.val), eng.n, 1, ptr(eng.y), 0,
                          eng.n, 1.0, None, ptr(eng.attr), st)
 
+    def step_forces(mode):
+        # the engine's entry point over the whole share (one GPU)
+        call(fn("bh_step_forces"), t.sref(), ptr(eng.bounds),
+             float(args.theta), ptr(eng.y), ptr(eng.rank_of), None,
+             ptr(eng.part), eng.cap, mode, ptr(eng.rep), ptr(eng.zpart),
+             ptr(eng.ws_rep), eng.ws_rep.numel(), ptr(eng.rp), ptr(eng.col),
+             ptr(eng.val), 1, ptr(eng.sched), ptr(eng.attr), st)
+
     def sort_build():
         call("bh_sort", ptr(eng.codes), eng.n, 32, ptr(t.sorted_codes),
              ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st)
@@ -109,6 +117,7 @@ def child(args):
            "repulsive_ms": timeit(rep, args.reps),
            "forces_fused_ms": timeit(fused, args.reps),
            "sort_build_ms": timeit(sort_build, args.reps),
+
            "sort_ms": timeit(lambda: call(
                "bh_sort", ptr(eng.codes), eng.n, 32, ptr(t.sorted_codes),
                ptr(t.order), ptr(eng.ws_sort), eng.ws_sort.numel(), st),
@@ -134,6 +143,12 @@ def child(args):
                                             args.reps)
         out["tree_build_prefix_ms"] = timeit(
             lambda: (t.build(eng.y), t.summarize_prefix()), args.reps)
+    # the engine's force entry point on a complete tree of this state
+    # (traversal of all points; fused with the sweep of rows [split, n))
+    eng.begin()
+    build()
+    out["step_traversal_ms"] = timeit(lambda: step_forces(1), args.reps)
+    out["step_fused_ms"] = timeit(lambda: step_forces(0), args.reps)
     print(json.dumps(out), flush=True)
 
 

@@ -130,7 +130,14 @@ def main():
     ap.add_argument("--bw", type=float, default=700.0,
                     help="NVLink 5 bus bandwidth per GPU in a collective, GB/s")
     ap.add_argument("--lat_us", type=float, default=10.0)
+    ap.add_argument("--splits", default=None,
+                    help="comma-separated side-sweep fractions to time per G "
+                         "(default: the engine's own choice)")
+    ap.add_argument("--worlds", default="1,2,4,8")
     args = ap.parse_args()
+    worlds = [int(x) for x in args.worlds.split(",")]
+    splits = ([float(x) for x in args.splits.split(",")] if args.splits
+              else [None])
     torch.cuda.set_device(0)
     prob = bench.problem("c3", torch.device("cuda", 0))
     p = bh.from_csr(prob["row_offsets"], prob["col"], prob["val"])
@@ -145,18 +152,21 @@ def main():
                        "Y (8 B/pt), ring/NVLS cost 2(G-1)/G and (G-1)/G of "
                        "the buffer at bw, plus lat_us each"}}
     base = None
-    for world in (1, 2, 4, 8):
+    for world, split in [(w, sp) for w in worlds for sp in splits]:
         worst, per_rank, stage_rows = 0.0, [], []
         for r in range(world):
             e2 = bh.Embedding(y=e.y.clone(), v=e.v.clone(), g=e.g.clone(),
                               iteration=e.iteration)
             shard = None if world == 1 else stand_in_shard(r, world)
             eng = bh.Engine(p, e2, cfg, shard=shard)
+            if split is not None:
+                eng.attr_split = split
             eng.run(1)           # builds a tree of this state
             eng.relabel()        # storage = tree order, shares re-balanced
             eng.begin()          # bounds of the centred Y, no pending shift
             torch.cuda.synchronize()
             ms, stages = time_iteration(eng, args.reps)
+            eng_split = eng.attr_split
             per_rank.append(ms)
             stage_rows.append({k: round(v, 4) for k, v in stages.items()})
             worst = max(worst, ms)
@@ -170,12 +180,14 @@ def main():
         step = worst + comm_ms
         if base is None:
             base = step
-        out[f"G{world}"] = {"per_rank_ms": per_rank, "max_rank_ms": worst,
+        key = f"G{world}" if split is None else f"G{world}_split{split:g}"
+        out[key] = {"attr_split": eng_split, "per_rank_ms": per_rank,
+                            "max_rank_ms": worst,
                             "stages_ms_rank0": stage_rows[0],
                             "comm_model_ms": comm_ms, "step_ms": step,
                             "projected_it_s": 1e3 / step,
                             "speedup_vs_1": base / step}
-        print(json.dumps({world: out[f"G{world}"]}), flush=True)
+        print(json.dumps({key: out[key]}), flush=True)
     print(json.dumps(out), flush=True)
 
 
