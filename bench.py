@@ -952,7 +952,7 @@ def main():
                     help="end-to-end runs through the public API (median)")
     ap.add_argument("--ref-max-steps", type=int, default=200,
                     help="cap of the reference arm's timed steps (0: none)")
-    ap.add_argument("--relabel-every", type=int, default=50,
+    ap.add_argument("--relabel-every", type=int, default=100,
                     help="Morton relabeling period of the engine (0: never)")
     ap.add_argument("--attr-split", type=float, default=None,
                     help="fraction of CSR rows swept under the tree build")

@@ -22,7 +22,7 @@ north star:
   independent of the GPU count.
 
 Velocity and gains stay sharded; they are gathered only when the storage
-order is renumbered (relabel, every 50 iterations) and at the end of a run.
+order is renumbered (relabel, every relabel_every = 100 iterations) and at the end of a run.
 
 ``Shard`` binds this to the CUDA engine through a small collective
 interface: ``NcclComm`` (torch.distributed, the product path, captured in

@@ -70,7 +70,7 @@ class TsneConfig:
     kl_every: int = 0
     code_bits: int = DEFAULT_CODE_BITS
     graph_chunk: int = 25
-    relabel_every: int = 50  # Morton renumbering period (0: never)
+    relabel_every: int = 100  # tree-order renumbering period (0: never)
     # the engine's tree order: "hilbert" keys (the same cells and leaves as
     # the reference's Morton tree, siblings along the Hilbert curve: no
     # jumps between consecutive points, 6.5% faster traversal at C3) or
