@@ -366,33 +366,6 @@ int bh_step_attractive(const int64_t *row_ptr, const int32_t *col,
                        const bh_part_t *part, int64_t max_rows,
                        const bh_sched_t *sched, float *attr,
                        bh_stream_t stream);
-/* Staged CSR sweep (forces.py:56-72, the y[j] gathers of attractive()).
- * P is static between relabels: bh_attr_stage_build gives every block of
- * rows_per_block consecutive rows the sorted list of the distinct columns
- * its entries name (ucol[b * slots ..], ucount[b] <= slots) and every padded
- * CSR entry its 16-bit position in that list (slot[q]; 0xFFFF = beyond the
- * list, read through col[q]).  bh_attractive_staged / bh_step_attractive_staged
- * are bh_attractive / bh_step_attractive with the block's distinct y_j
- * gathered once into shared memory (slots * 8 bytes per CTA) and read by
- * slot: same lanes, entries and summation order, bitwise the same result.
- * Padded float32 CSR only. */
-int bh_attr_stage_build(const int64_t *row_ptr, const int32_t *col, int64_t n,
-                        int rows_per_block, int slots, int32_t *ucol,
-                        int32_t *ucount, uint16_t *slot, bh_stream_t stream);
-int bh_attractive_staged(const int64_t *row_ptr, const int32_t *col,
-                         const float *val, const uint16_t *slot,
-                         const int32_t *ucol, const int32_t *ucount,
-                         int rows_per_block, int slots, const float *y,
-                         int64_t row_begin, int64_t row_end,
-                         float exaggeration, const bh_sched_t *sched,
-                         float *attr, bh_stream_t stream);
-int bh_step_attractive_staged(const int64_t *row_ptr, const int32_t *col,
-                              const float *val, const uint16_t *slot,
-                              const int32_t *ucol, const int32_t *ucount,
-                              int rows_per_block, int slots, const float *y,
-                              const bh_part_t *part, int64_t max_rows,
-                              const bh_sched_t *sched, float *attr,
-                              bh_stream_t stream);
 size_t bh_step_qlist_workspace_bytes(int64_t n);
 int bh_step_qlist(const int32_t *order, int64_t n, const bh_part_t *part,
                   int32_t *qlist, void *ws, size_t ws_bytes,

@@ -13,7 +13,7 @@ INCLUDE = os.path.join(REPO, "include")
 OBJ = os.path.join(REPO, "build", "obj")
 LIB = os.path.join(HERE, "libbhtsne_b200.so")
 SOURCES = ["abi.cu", "points.cu", "sort.cu", "tree.cu", "forces.cu", "engine.cu",
-           "forces_f64.cu", "affinity.cu", "knn.cu", "stage.cu"]
+           "forces_f64.cu", "affinity.cu", "knn.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
          "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE,

@@ -134,12 +134,6 @@ SIGNATURES = {
     "bh_knn_general": ([_P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P], C.c_int),
     "bh_knn_general_f64": ([_P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P],
                            C.c_int),
-    "bh_attr_stage_build": ([_P, _P, _I64, C.c_int, C.c_int, _P, _P, _P, _P],
-                            C.c_int),
-    "bh_attractive_staged": ([_P, _P, _P, _P, _P, _P, C.c_int, C.c_int, _P,
-                              _I64, _I64, C.c_float, _P, _P, _P], C.c_int),
-    "bh_step_attractive_staged": ([_P, _P, _P, _P, _P, _P, C.c_int, C.c_int,
-                                   _P, _P, _I64, _P, _P, _P], C.c_int),
     "bh_gather_rows": ([_P, _P, _I64, C.c_int, _P, _P], C.c_int),
     "bh_scatter_rows": ([_P, _P, _I64, C.c_int, _P, _P], C.c_int),
     "bh_invert_perm": ([_P, _I64, _P, _P], C.c_int),
