@@ -162,8 +162,9 @@ def problem(config: str, dev):
     out = dict(n=np.array(x.shape[0]), row_offsets=ro, col=co, val=va,
                y0=init_y0(x.shape[0], 0))
     try:
-        np.savez(path + ".tmp.npz", **out)
-        os.replace(path + ".tmp.npz", path)
+        tmp = f"{path}.{os.getpid()}.tmp.npz"  # one writer per file
+        np.savez(tmp, **out)
+        os.replace(tmp, path)
     except OSError:
         pass
     return out
@@ -479,6 +480,12 @@ def ours_arm(args, rank, world):
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        # rank 0 builds (and caches) the inputs, the others load its cache:
+        # no N-fold kNN / host BSP, no concurrent writers of the cache file
+        if rank == 0:
+            problem(args.config, dev)
+        dist.barrier()
     prob = problem(args.config, dev)
     n = int(prob["n"])
     nnz = int(prob["col"].shape[0])
