@@ -1,5 +1,5 @@
-import sys
+"""`python -m paper_2212_11506_b200 embed|profile|kl ...` (the CLI in cli.py)."""
 
-from .cli import main
+from paper_2212_11506_b200 import cli
 
-sys.exit(main())
+raise SystemExit(cli.main())
