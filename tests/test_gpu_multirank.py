@@ -143,3 +143,36 @@ def test_nccl_collectives_in_graphs(bh):
     assert r.returncode == 0, r.stderr[-3000:]
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out == {"graphs_ok": True, "equal": True, "finite": True}, (out, r.stderr[-2000:])
+
+
+def test_nccl_multi_gpu_bitwise(bh):
+    """One rank per GPU over NCCL (torchrun), world 2 (and 4 when the box
+    has them): the sharded engine's trajectory equals the single-GPU one
+    bitwise on every rank.  Needs >= 2 GPUs (skipped on one-GPU boxes, where
+    dist.LocalGroup covers world 2 / 4 above)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    import pytest
+    import torch
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs >= 2 GPUs")
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                         "nccl_world1_child.py")
+    for world in [w for w in (2, 4) if w <= ngpu]:
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        r = subprocess.run(
+            [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+             f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+             "--master-port", str(port), child],
+            capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+        out = json.loads(line)
+        assert out["equal"] and out["finite"], (world, out, r.stderr[-2000:])
