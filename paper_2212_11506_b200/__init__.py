@@ -14,6 +14,7 @@ from .affinity import (NeighborGraph, PerplexityResult, SparseAffinity,
                        calibrate_perplexity, from_csr, set_exaggeration,
                        symmetrize)
 from .estimator import BarnesHutTSNE
+from .io import InputMatrix, load_labels, load_matrix, save_matrix
 from .forces import (GradientBuffers, attractive, repulsive_bh,
                      repulsive_counts, repulsive_exact)
 from .knn import knn_exact
@@ -25,7 +26,8 @@ from .quadtree import (MortonCodes, MortonQuadtree, build_tree,
                        summarize)
 
 __all__ = [
-    "__version__", "NeighborGraph", "PerplexityResult", "SparseAffinity",
+    "__version__", "InputMatrix", "load_matrix", "save_matrix",
+    "load_labels", "NeighborGraph", "PerplexityResult", "SparseAffinity",
     "calibrate_perplexity", "symmetrize", "set_exaggeration", "from_csr",
     "MortonCodes", "MortonQuadtree", "compute_bounds", "morton_codes",
     "morton_interleave", "build_tree", "summarize", "GradientBuffers",

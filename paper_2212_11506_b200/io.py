@@ -154,3 +154,20 @@ def save_matrix(m, path, format: str | None = None) -> None:
         write_csv(arr, path)
     else:
         raise ValueError(f"unknown format {fmt!r}; expected 'csv' or 'bin'")
+
+
+def load_labels(path) -> np.ndarray:
+    """One integer class id per non-empty line -- the first comma-separated
+    field, "3" and "3.0" alike (io.py:120-128; used by the plot only)."""
+    ids = []
+    with open(path) as fh:
+        for lineno, line in enumerate(fh, start=1):
+            field = line.strip().split(",")[0]
+            if not line.strip():
+                continue
+            try:
+                ids.append(int(float(field)))
+            except ValueError:
+                raise ValueError(f"labels file {path}: line {lineno}: "
+                                 f"{field!r} is not a class id") from None
+    return np.asarray(ids, dtype=np.int64)

@@ -23,6 +23,20 @@ def test_bhtm_bytes_match_the_reference_layout(tmp_path):
     np.testing.assert_array_equal(io.load_matrix(p, precision="f64").data, b)
 
 
+def test_labels_and_package_exports(tmp_path):
+    # io.py:120-128: one class id per non-empty line, first CSV field
+    p = tmp_path / "labels.txt"
+    p.write_text("3\n\n1.0,extra\n 7 \n")
+    np.testing.assert_array_equal(io.load_labels(p), [3, 1, 7])
+    assert io.load_labels(p).dtype == np.int64
+    p.write_text("2\nnot-a-label\n")
+    with pytest.raises(ValueError, match="labels file"):
+        io.load_labels(p)
+    import paper_2212_11506_b200 as pkg
+    for name in ("InputMatrix", "load_matrix", "save_matrix", "load_labels"):
+        assert getattr(pkg, name) is getattr(io, name) and name in pkg.__all__
+
+
 def test_csv_round_trip_and_errors(tmp_path):
     a = np.random.default_rng(0).standard_normal((5, 3))
     p = tmp_path / "m.csv"
