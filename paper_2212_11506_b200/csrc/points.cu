@@ -195,6 +195,11 @@ k_bounds(const p2_t<T> *__restrict__ y, int64_t n, int code_bits,
     }
 }
 
+#ifndef BH_HILBERT_LUT
+// Hilbert keys four levels per shared-memory table lookup (keys.cuh); 0
+// keeps the level-by-level walk (A/B builds)
+#define BH_HILBERT_LUT 1
+#endif
 template <int BITS, typename T, bool HILBERT = false>
 __global__ void __launch_bounds__(kPtThreads)
 k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
@@ -204,6 +209,8 @@ k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
     bh_pdl_trigger();  // the successor may launch early (PDL)
     bh_pdl_wait();     // the predecessor's results are visible
 
+    __shared__ uint16_t s_lut[HILBERT && BH_HILBERT_LUT ? 1024 : 1];
+    if (HILBERT && BH_HILBERT_LUT) hilbert_lut_load(s_lut);
     const double root0 = b->root0, root1 = b->root1, scale = b->scale;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -212,8 +219,12 @@ k_morton(p2_t<T> *__restrict__ y, int64_t n, const bh_bounds_t *__restrict__ b,
             p = shifted(p, b);
             y[i] = p;
         }
-        codes[i] = point_key<BITS, HILBERT>((double)p.x, (double)p.y, root0,
-                                             root1, scale);
+        if (HILBERT && BH_HILBERT_LUT)
+            codes[i] = point_key_hilbert_lut<BITS>((double)p.x, (double)p.y,
+                                                   root0, root1, scale, s_lut);
+        else
+            codes[i] = point_key<BITS, HILBERT>((double)p.x, (double)p.y,
+                                                root0, root1, scale);
     }
 }
 

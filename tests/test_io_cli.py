@@ -89,3 +89,106 @@ def test_cli_embed_writes_embedding_manifest_timings(tmp_path):
     assert main(["embed", "--input", str(inp), "--out", str(out2),
                  "--from-manifest", str(tmp_path / "y.bin.manifest.json")]) == 0
     assert out2.read_bytes() == out.read_bytes()
+
+
+# --- the reference's CLI tests (pkg/tests/test_cli.py), restated -------------
+
+@pytest.fixture
+def cli(tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2212_11506_b200.cli import main
+    rng = np.random.default_rng(11)
+    centres = np.array([[0.0, 0.0, 0.0], [8.0, 8.0, 8.0]])
+    pts = np.vstack([c + rng.standard_normal((30, 3)) for c in centres])
+    data = tmp_path / "data.csv"
+    io.save_matrix(pts, data, format="csv")
+
+    def embed_args(out, **extra):
+        args = ["embed", "--input", str(data), "--out", str(out),
+                "--perplexity", "5", "--iters", "50",
+                "--exaggeration-iters", "20", "--seed", "1"]
+        for key, val in extra.items():
+            args += [f"--{key.replace('_', '-')}", str(val)]
+        return args
+    return main, data, embed_args
+
+
+@pytest.mark.gpu
+def test_cli_embed_outputs_and_exit_codes(cli, tmp_path, capsys):
+    from paper_2212_11506_b200.optimizer import STAGES
+    main, data, embed_args = cli
+    out = tmp_path / "emb.csv"
+    assert main(embed_args(out)) == 0
+    emb = io.load_matrix(out, format="csv")
+    assert (emb.n_points, emb.n_dims) == (60, 2)
+    m = json.loads((tmp_path / "emb.csv.manifest.json").read_text())
+    assert np.isfinite(m["kl"]) and m["seed"] == 1 and m["input"]["sha256"]
+    t = json.loads((tmp_path / "emb.csv.timings.json").read_text())
+    assert set(t) == set(STAGES)            # exactly the reference's stages
+    assert "forces" in m["engine_timings"]
+    # usage errors exit 2 with the reason, run-time errors return 1
+    with pytest.raises(SystemExit) as exc:
+        main(embed_args(tmp_path / "e.csv", perplexity="0.5"))
+    assert exc.value.code == 2
+    err = capsys.readouterr().err
+    assert "perplexity" in err and "> 1" in err
+    rc = main(["embed", "--input", str(tmp_path / "nope.csv"),
+               "--out", str(tmp_path / "e.csv")])
+    assert rc == 1 and "error" in capsys.readouterr().err
+    # --threads is accepted and changes nothing (test_cli.py:59-65)
+    outs = []
+    for threads in (1, 8):
+        o = tmp_path / f"emb{threads}.bin"
+        assert main(embed_args(o, threads=threads)) == 0
+        outs.append(o.read_bytes())
+    assert outs[0] == outs[1]
+
+
+@pytest.mark.gpu
+def test_cli_profile_table_and_json(cli, tmp_path, capsys):
+    from paper_2212_11506_b200.optimizer import STAGES
+    main, data, _ = cli
+    tj = tmp_path / "timings.json"
+    assert main(["profile", "--input", str(data), "--perplexity", "5",
+                 "--iters", "30", "--exaggeration-iters", "10",
+                 "--timings-out", str(tj)]) == 0
+    out = capsys.readouterr().out
+    lines = [ln for ln in out.splitlines() if ln and not ln.startswith("wall")]
+    body = [ln for ln in lines[1:] if not ln.startswith("total")]
+    assert [ln.split()[0] for ln in body] == list(STAGES)
+    pcts = [float(ln.split()[-1].rstrip("%")) for ln in body]
+    assert abs(sum(pcts) - 100.0) <= 0.5
+    report = json.loads(tj.read_text())
+    assert set(report) == set(STAGES)
+    for s in STAGES:
+        assert report[s]["total_s"] >= 0
+    # separate, non-overlapping kernels: every stage ran every iteration
+    for s in ("tree", "summarize", "attractive", "repulsive", "update"):
+        assert report[s]["calls"] == 30 and report[s]["total_s"] > 0
+
+
+@pytest.mark.gpu
+def test_cli_kl_matches_manifest_and_errors(cli, tmp_path, capsys):
+    main, data, embed_args = cli
+    out = tmp_path / "emb.bin"
+    assert main(embed_args(out)) == 0
+    m = json.loads((tmp_path / "emb.bin.manifest.json").read_text())
+    capsys.readouterr()
+    jout = tmp_path / "kl.json"
+    printed = []
+    for _ in range(2):
+        assert main(["kl", "--input", str(data), "--embedding", str(out),
+                     "--perplexity", "5", "--json-out", str(jout)]) == 0
+        printed.append(capsys.readouterr().out)
+    assert printed[0] == printed[1]                     # deterministic
+    assert f"kl={m['kl']:.6f}" in printed[0]
+    assert abs(json.loads(jout.read_text())["kl"] - m["kl"]) <= 1e-9
+    short = tmp_path / "short.csv"
+    io.save_matrix(np.random.default_rng(0).standard_normal((10, 2)), short,
+                   format="csv")
+    rc = main(["kl", "--input", str(data), "--embedding", str(short),
+               "--perplexity", "5"])
+    err = capsys.readouterr().err
+    assert rc == 1 and "10" in err and "60" in err
