@@ -174,6 +174,24 @@ def problem(config: str, dev):
 # clocks during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
+    """SM clock and clock-event reasons of one GPU during a timed region.
+
+    NVML is polled from a thread every few milliseconds (the driver's window,
+    20 iterations, lasts ~30 ms: `nvidia-smi -lms` cannot even start in that
+    time); without the NVML binding, `nvidia-smi -lms 100` is the fallback.
+    """
+
+    PERIOD_S = 0.004
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown",
+                "nvmlClocksThrottleReasonHwSlowdown"),
+               ("hw_thermal_slowdown",
+                "nvmlClocksEventReasonHwThermalSlowdown",
+                "nvmlClocksThrottleReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown",
+                "nvmlClocksEventReasonSwThermalSlowdown",
+                "nvmlClocksThrottleReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap",
+                "nvmlClocksThrottleReasonSwPowerCap"))
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,"
               "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,"
@@ -182,16 +200,75 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.rows = []
+        self.sm, self.reasons, self.sm_max = [], set(), None
+        self.rows = []          # nvidia-smi fallback
         self.proc = None
+        self.nvml = self.handle = None
+        self.stop = threading.Event()
+        self.source = None
 
+    # -- NVML ---------------------------------------------------------------
+    def _open_nvml(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            handle = None
+            try:  # the CUDA device's own UUID (CUDA_VISIBLE_DEVICES-proof)
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.gpu).uuid)
+                if not uuid.startswith("GPU-"):
+                    uuid = "GPU-" + uuid
+                handle = nv.nvmlDeviceGetHandleByUUID(uuid)
+            except Exception:  # noqa: BLE001 - older torch / NVML: by index
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                ids = [v for v in vis.split(",") if v.strip().isdigit()]
+                idx = int(ids[self.gpu]) if self.gpu < len(ids) else self.gpu
+                handle = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml, self.handle = nv, handle
+            self.sm_max = float(nv.nvmlDeviceGetMaxClockInfo(
+                handle, nv.NVML_CLOCK_SM))
+            self._masks = [(name, getattr(nv, a, None) or getattr(nv, b, 0))
+                           for name, a, b in self.REASONS]
+            self._get_reasons = getattr(
+                nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+            self._sample()      # fails here, not in the thread
+            self.sm.clear()
+            self.reasons.clear()
+            return True
+        except Exception:  # noqa: BLE001 - no binding / no NVML: fall back
+            self.nvml = self.handle = None
+            return False
+
+    def _sample(self):
+        nv, h = self.nvml, self.handle
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        if self._get_reasons is not None:
+            bits = int(self._get_reasons(h))
+            self.reasons.update(n for n, m in self._masks if m and bits & m)
+
+    def _poll(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001 - keep what was sampled
+                return
+            self.stop.wait(self.PERIOD_S)
+
+    # -- context ------------------------------------------------------------
     def __enter__(self):
+        if self._open_nvml():
+            self.source = "nvml"
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}",
                  f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except FileNotFoundError:
@@ -203,6 +280,9 @@ class ClockSampler:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1.0)
         if self.proc:
             self.proc.terminate()
             try:
@@ -211,6 +291,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nvml is not None and self.sm:
+            return {"sm_mhz": statistics.median(self.sm),
+                    "sm_max_mhz": self.sm_max,
+                    "reasons": sorted(self.reasons),
+                    "samples": len(self.sm), "source": "nvml"}
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
@@ -221,7 +306,7 @@ class ClockSampler:
                           if len(r) > 5 + j and r[5 + j].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
