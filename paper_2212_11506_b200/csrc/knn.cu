@@ -170,6 +170,210 @@ k_knn_f32(const float *__restrict__ x, int64_t n, int d, int k,
     }
 }
 
+// float32 data, register-tiled dot-product filter (the default for bh_knn).
+// k_knn_f32 spends one shared-memory operand (a 512-B register write-back)
+// per FMA, which caps it at a quarter of the FP32 rate; here a CTA of 128
+// threads filters 128 queries x 64 candidates per step as a small GEMM --
+// every thread an 8 x 8 tile of dot products, its operands (2 + 2 LDS.128
+// per column) reused 8 times.
+//
+// Filter bound: d^2 = |q|^2 + |s|^2 - 2 q.s.  With the f32 FMA sums nq, ns,
+// dot (each within gamma = D 2^-24 / (1 - D 2^-24) of its exact value
+// relative to the sum of magnitudes; |q.s| <= (|q|^2 + |s|^2) / 2) the exact
+// distance obeys d^2 >= (nq + ns)(1 - 2 gamma - gamma^2) - 2 dot, and the
+// three f32 operations evaluating the right-hand side add at most
+// 4 * 2^-24 (nq + ns).  kappa = 1e-5 exceeds 2 gamma + gamma^2 + 4 * 2^-24
+// for D <= 64, so a candidate with (nq + ns)(1 - kappa) - 2 dot > thr (the
+// query's current k-th exact distance, rounded up) cannot enter its list.
+// Every other candidate is flagged in the query's 64-bit pass mask; after
+// the step the query's owner thread takes them in ascending id order
+// through k_knn's exact f64 column-order sum and strict-less insertion, so
+// the kept set, the distances and the tie order are k_knn's, bit for bit.
+// The filter is weakest (never wrong) for data far from the origin.
+constexpr int kTileQ = 128, kTileC = 64;   // CTA tile (queries x candidates)
+constexpr int kTileCS = kTileC + 4;        // candidate row stride (words)
+constexpr float kKnnKappa = 1e-5f;
+
+template <int DMAX>
+struct KnnTileSmem {
+    float q[DMAX][kTileQ];    // queries, transposed
+    float c[DMAX][kTileCS];   // candidates, transposed
+    float nq[kTileQ], thr[kTileQ], nc[kTileC];
+    unsigned mask[kTileQ][2];
+};
+
+template <int DMAX>
+__global__ void __launch_bounds__(kTileQ)
+k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
+           int64_t *__restrict__ out_idx, float *__restrict__ out_sqd) {
+    extern __shared__ __align__(16) unsigned char knn_smem[];
+    KnnTileSmem<DMAX> &S = *reinterpret_cast<KnnTileSmem<DMAX> *>(knn_smem);
+    const int tid = threadIdx.x;
+    const int64_t q0 = blockIdx.x * (int64_t)kTileQ;
+    const int64_t i = q0 + tid;  // the query this thread owns
+    const bool ok = i < n;
+    // the query tile, transposed (once per CTA), norms and thresholds
+    for (int e = tid; e < kTileQ * DMAX; e += kTileQ) {
+        const int r = e / DMAX, c = e % DMAX;
+        S.q[c][r] = (q0 + r < n && c < d) ? x[(q0 + r) * d + c] : 0.f;
+    }
+    S.thr[tid] = INFINITY;
+    S.mask[tid][0] = S.mask[tid][1] = 0u;
+    __syncthreads();
+    {
+        float a = 0.f;
+#pragma unroll
+        for (int c = 0; c < DMAX; c++) a = fmaf(S.q[c][tid], S.q[c][tid], a);
+        S.nq[tid] = a;
+    }
+    double bd[kKnnMaxK];
+    int32_t bi[kKnnMaxK];
+    for (int t = 0; t < k; t++) {
+        bd[t] = INFINITY;
+        bi[t] = -1;
+    }
+    double thr = INFINITY;
+    // this thread's 8 x 8 tile: queries tq4 + {0..3}, 64 + tq4 + {0..3},
+    // candidates tc4 + {0..3}, 32 + tc4 + {0..3} (conflict-free LDS.128)
+    const int tq4 = (tid & 15) * 4, tc4 = (tid >> 4) * 4;
+    const float om = 1.0f - kKnnKappa;
+    for (int64_t j0 = 0; j0 < n; j0 += kTileC) {
+        __syncthreads();  // the previous step's owners are done with S.c
+        for (int e = tid; e < kTileC * DMAX; e += kTileQ) {
+            const int r = e / DMAX, c = e % DMAX;
+            const int64_t j = j0 + r;
+            S.c[c][r] = (j < n && c < d) ? x[j * d + c] : 0.f;
+        }
+        __syncthreads();
+        if (tid < kTileC) {
+            float a = 0.f;
+#pragma unroll
+            for (int c = 0; c < DMAX; c++) a = fmaf(S.c[c][tid], S.c[c][tid], a);
+            S.nc[tid] = j0 + tid < n ? a : INFINITY;  // past the end: never passes
+        }
+        float acc[8][8];
+#pragma unroll
+        for (int a = 0; a < 8; a++)
+#pragma unroll
+            for (int b = 0; b < 8; b++) acc[a][b] = 0.f;
+#pragma unroll 4
+        for (int c = 0; c < DMAX; c++) {
+            const float4 qa = *reinterpret_cast<const float4 *>(&S.q[c][tq4]);
+            const float4 qb = *reinterpret_cast<const float4 *>(&S.q[c][64 + tq4]);
+            const float4 ca = *reinterpret_cast<const float4 *>(&S.c[c][tc4]);
+            const float4 cb = *reinterpret_cast<const float4 *>(&S.c[c][32 + tc4]);
+            const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+            const float cv[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int b = 0; b < 8; b++)
+                    acc[a][b] = fmaf(qv[a], cv[b], acc[a][b]);
+        }
+        __syncthreads();  // S.nc is written
+        // filter: flag the pairs that may enter
+#pragma unroll
+        for (int a = 0; a < 8; a++) {
+            const int ql = (a < 4 ? tq4 : 60 + tq4) + a;  // 64 + tq4 + (a - 4)
+            const float nqa = S.nq[ql], th = S.thr[ql];
+            unsigned m0 = 0u, m1 = 0u;
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                const int cl = (b < 4 ? tc4 : 28 + tc4) + b;  // 32 + tc4 + (b - 4)
+                const float lower =
+                    fmaf(nqa + S.nc[cl], om, -2.0f * acc[a][b]);
+                if (!(lower > th)) {
+                    if (b < 4) m0 |= 1u << cl;
+                    else m1 |= 1u << (cl - 32);
+                }
+            }
+            if (m0) atomicOr(&S.mask[ql][0], m0);
+            if (m1) atomicOr(&S.mask[ql][1], m1);
+        }
+        __syncthreads();
+        // the owner inserts its query's flagged candidates, ascending id
+        if (ok) {
+#pragma unroll 1
+            for (int h = 0; h < 2; h++) {
+                unsigned m = S.mask[tid][h];
+                if (m == 0u) continue;
+                S.mask[tid][h] = 0u;
+                while (m) {
+                    const int r = 32 * h + __ffs(m) - 1;
+                    m &= m - 1;
+                    const int64_t j = j0 + r;
+                    if (j == i || j >= n) continue;
+                    // exact: f64, column order, no FMA (knn.py:36-59).
+                    // Unrolled over the padded width (the loads and products
+                    // overlap; only the ordered sum is a chain): columns past
+                    // d are 0 in both tiles and add an exact +0.
+                    double e = 0.0;
+#pragma unroll
+                    for (int c = 0; c < DMAX; c++) {
+                        const double diff = __dsub_rn((double)S.q[c][tid],
+                                                      (double)S.c[c][r]);
+                        e = __dadd_rn(e, __dmul_rn(diff, diff));
+                    }
+                    if (!(e < thr)) continue;
+                    // strict-less insertion: before the first entry > e
+                    // (bd[k - 1] > e here), found by bisection; then the
+                    // tail moves up one slot, four entries per round trip
+                    int lo = 0, hi = k - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (bd[mid] > e) hi = mid;
+                        else lo = mid + 1;
+                    }
+                    const int pos = lo;
+                    int t = k - 1;
+                    for (; t - 4 >= pos; t -= 4) {
+                        const double d0 = bd[t - 1], d1 = bd[t - 2],
+                                     d2 = bd[t - 3], d3 = bd[t - 4];
+                        const int32_t i0 = bi[t - 1], i1 = bi[t - 2],
+                                      i2 = bi[t - 3], i3 = bi[t - 4];
+                        bd[t] = d0; bd[t - 1] = d1; bd[t - 2] = d2; bd[t - 3] = d3;
+                        bi[t] = i0; bi[t - 1] = i1; bi[t - 2] = i2; bi[t - 3] = i3;
+                    }
+                    for (; t > pos; t--) {
+                        bd[t] = bd[t - 1];
+                        bi[t] = bi[t - 1];
+                    }
+                    bd[pos] = e;
+                    bi[pos] = (int32_t)j;
+                    thr = bd[k - 1];
+                }
+            }
+            S.thr[tid] = __double2float_ru(__dmul_ru(thr, 1.0 + 1e-6));
+        } else {
+            S.mask[tid][0] = S.mask[tid][1] = 0u;
+        }
+    }
+    if (ok) {
+        for (int t = 0; t < k; t++) {
+            out_idx[i * k + t] = bi[t];
+            out_sqd[i * k + t] = (float)bd[t];
+        }
+    }
+}
+
+template <int DMAX>
+static int knn_tile_launch(const float *x, int64_t n, int d, int k,
+                           int64_t *out_idx, float *out_sqd, cudaStream_t st) {
+    const size_t smem = sizeof(KnnTileSmem<DMAX>);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(
+            k_knn_tile<DMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            (int)smem);
+        if (e != cudaSuccess) return cuda_status(e, "k_knn_tile smem");
+        attr_set = true;
+    }
+    k_knn_tile<DMAX><<<bh_blocks(n, kTileQ), kTileQ, smem, st>>>(
+        x, n, d, k, out_idx, out_sqd);
+    BH_CHECK_LAUNCH("k_knn_tile");
+    return BH_OK;
+}
+
 // Any D, any k (bh_knn_general): the same arithmetic and insertion rule,
 // with the query's columns streamed in chunks of kKnnChunk (a tile of 32
 // candidate rows per chunk in shared memory, one f64 partial sum per
@@ -303,6 +507,21 @@ static int knn_impl(const T *x, int64_t n, int64_t d, int64_t k,
     if (std::is_same<T, float>::value && knn_f32_filter()) {
         const float *xf = (const float *)x;
         float *of = (float *)out_sqd;
+        static const bool tile = [] {  // BH_KNN_TILE=0: the per-thread filter
+            const char *s = getenv("BH_KNN_TILE");
+            return s ? atoi(s) != 0 : true;
+        }();
+        if (tile) {
+            const int di = (int)d, ki = (int)k;
+            if (d <= 8) return knn_tile_launch<8>(xf, n, di, ki, out_idx, of, st);
+            if (d <= 16) return knn_tile_launch<16>(xf, n, di, ki, out_idx, of, st);
+            if (d <= 24) return knn_tile_launch<24>(xf, n, di, ki, out_idx, of, st);
+            if (d <= 32) return knn_tile_launch<32>(xf, n, di, ki, out_idx, of, st);
+            if (d <= 40) return knn_tile_launch<40>(xf, n, di, ki, out_idx, of, st);
+            if (d <= 48) return knn_tile_launch<48>(xf, n, di, ki, out_idx, of, st);
+            if (d <= 56) return knn_tile_launch<56>(xf, n, di, ki, out_idx, of, st);
+            return knn_tile_launch<64>(xf, n, di, ki, out_idx, of, st);
+        }
         // row widths in steps of 8 (the filter's predicated columns issue
         // whether or not they exist)
         if (d <= 16)
