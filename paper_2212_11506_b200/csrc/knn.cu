@@ -191,13 +191,28 @@ k_knn_f32(const float *__restrict__ x, int64_t n, int d, int k,
 // the kept set, the distances and the tie order are k_knn's, bit for bit.
 // The filter is weakest (never wrong) for data far from the origin.
 constexpr int kTileQ = 128, kTileC = 64;   // CTA tile (queries x candidates)
-constexpr int kTileCS = kTileC + 4;        // candidate row stride (words)
 constexpr float kKnnKappa = 1e-5f;
+
+// 4-byte asynchronous global -> shared copy (zero fill when !valid)
+__device__ __forceinline__ void cp_async4(float *smem_dst, const float *gsrc,
+                                          bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const int sz = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa),
+                 "l"(gsrc), "r"(sz)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
 
 template <int DMAX>
 struct KnnTileSmem {
-    float q[DMAX][kTileQ];    // queries, transposed
-    float c[DMAX][kTileCS];   // candidates, transposed
+    float q[DMAX][kTileQ];       // queries, transposed
+    float c[2][kTileC][DMAX + 4];  // candidates (row-major), double-buffered
     float nq[kTileQ], thr[kTileQ], nc[kTileC];
     unsigned mask[kTileQ][2];
 };
@@ -237,18 +252,31 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
     // candidates tc4 + {0..3}, 32 + tc4 + {0..3} (conflict-free LDS.128)
     const int tq4 = (tid & 15) * 4, tc4 = (tid >> 4) * 4;
     const float om = 1.0f - kKnnKappa;
-    for (int64_t j0 = 0; j0 < n; j0 += kTileC) {
-        __syncthreads();  // the previous step's owners are done with S.c
-        for (int e = tid; e < kTileC * DMAX; e += kTileQ) {
-            const int r = e / DMAX, c = e % DMAX;
+    // candidate tiles arrive by cp.async one step ahead of their use
+    auto stage = [&](int64_t j0, int buf) {
+        // a warp copies whole rows (coalesced reads, conflict-free writes)
+        for (int r = tid >> 5; r < kTileC; r += kTileQ / 32) {
             const int64_t j = j0 + r;
-            S.c[c][r] = (j < n && c < d) ? x[j * d + c] : 0.f;
+#pragma unroll
+            for (int c = tid & 31; c < DMAX; c += 32) {
+                const bool in = j < n && c < d;
+                cp_async4(&S.c[buf][r][c], in ? x + j * d + c : x, in);
+            }
         }
-        __syncthreads();
+        cp_async_commit();
+    };
+    stage(0, 0);
+    int buf = 0;
+    for (int64_t j0 = 0; j0 < n; j0 += kTileC, buf ^= 1) {
+        cp_async_wait_all();
+        __syncthreads();  // this step's tile has landed; the previous step's
+                          // owners are done with the other buffer
+        if (j0 + kTileC < n) stage(j0 + kTileC, buf ^ 1);
+        const float (*Sc)[DMAX + 4] = S.c[buf];
         if (tid < kTileC) {
             float a = 0.f;
 #pragma unroll
-            for (int c = 0; c < DMAX; c++) a = fmaf(S.c[c][tid], S.c[c][tid], a);
+            for (int c = 0; c < DMAX; c++) a = fmaf(Sc[tid][c], Sc[tid][c], a);
             S.nc[tid] = j0 + tid < n ? a : INFINITY;  // past the end: never passes
         }
         float acc[8][8];
@@ -256,19 +284,30 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
         for (int a = 0; a < 8; a++)
 #pragma unroll
             for (int b = 0; b < 8; b++) acc[a][b] = 0.f;
-#pragma unroll 4
-        for (int c = 0; c < DMAX; c++) {
-            const float4 qa = *reinterpret_cast<const float4 *>(&S.q[c][tq4]);
-            const float4 qb = *reinterpret_cast<const float4 *>(&S.q[c][64 + tq4]);
-            const float4 ca = *reinterpret_cast<const float4 *>(&S.c[c][tc4]);
-            const float4 cb = *reinterpret_cast<const float4 *>(&S.c[c][32 + tc4]);
-            const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-            const float cv[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll 2
+        for (int c = 0; c < DMAX; c += 2) {
+            // two columns per round: 8 broadcast LDS.64 of the candidates'
+            // rows, 2 + 2 LDS.128 of the transposed queries
+            float2 cw[8];
 #pragma unroll
-            for (int a = 0; a < 8; a++)
+            for (int b = 0; b < 8; b++)
+                cw[b] = *reinterpret_cast<const float2 *>(
+                    &Sc[(b < 4 ? tc4 : 28 + tc4) + b][c]);
 #pragma unroll
-                for (int b = 0; b < 8; b++)
-                    acc[a][b] = fmaf(qv[a], cv[b], acc[a][b]);
+            for (int h = 0; h < 2; h++) {
+                const float4 qa =
+                    *reinterpret_cast<const float4 *>(&S.q[c + h][tq4]);
+                const float4 qb =
+                    *reinterpret_cast<const float4 *>(&S.q[c + h][64 + tq4]);
+                const float qv[8] = {qa.x, qa.y, qa.z, qa.w,
+                                     qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+                for (int a = 0; a < 8; a++)
+#pragma unroll
+                    for (int b = 0; b < 8; b++)
+                        acc[a][b] = fmaf(qv[a], h ? cw[b].y : cw[b].x,
+                                         acc[a][b]);
+            }
         }
         __syncthreads();  // S.nc is written
         // filter: flag the pairs that may enter
@@ -311,7 +350,7 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
 #pragma unroll
                     for (int c = 0; c < DMAX; c++) {
                         const double diff = __dsub_rn((double)S.q[c][tid],
-                                                      (double)S.c[c][r]);
+                                                      (double)Sc[r][c]);
                         e = __dadd_rn(e, __dmul_rn(diff, diff));
                     }
                     if (!(e < thr)) continue;
