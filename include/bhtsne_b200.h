@@ -486,7 +486,8 @@ int bh_permute_csr_f64(const int64_t *row_ptr, const int32_t *col,
  * x: (n, d) float32 row-major, d <= 64, k <= 128. */
 int bh_knn(const float *x, int64_t n, int64_t d, int64_t k, int64_t *out_idx,
            float *out_sqd, bh_stream_t stream);
-/* Any D and k (the same semantics and results as bh_knn; slower): the
+/* Any D and k (the same semantics and results as bh_knn; float32 rows of
+ * D <= 64 take bh_knn's tile filter for any k, the rest is slower): the
  * query's columns streamed in chunks, the running top-k in caller scratch of
  * bh_knn_general_workspace_bytes(n, k) bytes. */
 size_t bh_knn_general_workspace_bytes(int64_t n, int64_t k);

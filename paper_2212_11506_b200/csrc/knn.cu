@@ -217,10 +217,13 @@ struct KnnTileSmem {
     unsigned mask[kTileQ][2];
 };
 
-template <int DMAX>
+// KCAP: capacity of the thread-local top-k lists (k <= KCAP); 0 = the lists
+// live in caller scratch instead (any k).
+template <int DMAX, int KCAP>
 __global__ void __launch_bounds__(kTileQ)
 k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
-           int64_t *__restrict__ out_idx, float *__restrict__ out_sqd) {
+           int64_t *__restrict__ out_idx, float *__restrict__ out_sqd,
+           double *__restrict__ ws_d, int32_t *__restrict__ ws_i) {
     extern __shared__ __align__(16) unsigned char knn_smem[];
     KnnTileSmem<DMAX> &S = *reinterpret_cast<KnnTileSmem<DMAX> *>(knn_smem);
     const int tid = threadIdx.x;
@@ -241,12 +244,16 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
         for (int c = 0; c < DMAX; c++) a = fmaf(S.q[c][tid], S.q[c][tid], a);
         S.nq[tid] = a;
     }
-    double bd[kKnnMaxK];
-    int32_t bi[kKnnMaxK];
-    for (int t = 0; t < k; t++) {
-        bd[t] = INFINITY;
-        bi[t] = -1;
-    }
+    constexpr bool SCRATCH = KCAP == 0;
+    double bd_local[SCRATCH ? 1 : KCAP];
+    int32_t bi_local[SCRATCH ? 1 : KCAP];
+    double *bd = SCRATCH ? ws_d + (ok ? i : 0) * (int64_t)k : bd_local;
+    int32_t *bi = SCRATCH ? ws_i + (ok ? i : 0) * (int64_t)k : bi_local;
+    if (ok || !SCRATCH)
+        for (int t = 0; t < k; t++) {
+            bd[t] = INFINITY;
+            bi[t] = -1;
+        }
     double thr = INFINITY;
     // this thread's 8 x 8 tile: queries tq4 + {0..3}, 64 + tq4 + {0..3},
     // candidates tc4 + {0..3}, 32 + tc4 + {0..3} (conflict-free LDS.128)
@@ -395,22 +402,55 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
     }
 }
 
-template <int DMAX>
+template <int DMAX, int KCAP>
 static int knn_tile_launch(const float *x, int64_t n, int d, int k,
-                           int64_t *out_idx, float *out_sqd, cudaStream_t st) {
+                           int64_t *out_idx, float *out_sqd, double *ws_d,
+                           int32_t *ws_i, cudaStream_t st) {
     const size_t smem = sizeof(KnnTileSmem<DMAX>);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(
-            k_knn_tile<DMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-            (int)smem);
+            k_knn_tile<DMAX, KCAP>,
+            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_status(e, "k_knn_tile smem");
         attr_set = true;
     }
-    k_knn_tile<DMAX><<<bh_blocks(n, kTileQ), kTileQ, smem, st>>>(
-        x, n, d, k, out_idx, out_sqd);
+    k_knn_tile<DMAX, KCAP><<<bh_blocks(n, kTileQ), kTileQ, smem, st>>>(
+        x, n, d, k, out_idx, out_sqd, ws_d, ws_i);
     BH_CHECK_LAUNCH("k_knn_tile");
     return BH_OK;
+}
+
+// BH_KNN_TILE=0: the per-thread kernels instead of the tile filter (A/B)
+static bool knn_tile_filter() {
+    static const bool on = [] {
+        const char *s = getenv("BH_KNN_TILE");
+        return s ? atoi(s) != 0 : true;
+    }();
+    return on;
+}
+
+constexpr int kKnnBigK = 512;  // thread-local lists up to this k
+
+template <int KCAP>
+static int knn_tile_dispatch(const float *x, int64_t n, int64_t d, int64_t k,
+                             int64_t *out_idx, float *out_sqd, double *ws_d,
+                             int32_t *ws_i, cudaStream_t st) {
+    const int di = (int)d, ki = (int)k;
+#define BH_KNN_TILE_CASE(W)                                                   \
+    if (d <= W)                                                               \
+        return knn_tile_launch<W, KCAP>(x, n, di, ki, out_idx, out_sqd,       \
+                                        ws_d, ws_i, st)
+    BH_KNN_TILE_CASE(8);
+    BH_KNN_TILE_CASE(16);
+    BH_KNN_TILE_CASE(24);
+    BH_KNN_TILE_CASE(32);
+    BH_KNN_TILE_CASE(40);
+    BH_KNN_TILE_CASE(48);
+    BH_KNN_TILE_CASE(56);
+    BH_KNN_TILE_CASE(64);
+#undef BH_KNN_TILE_CASE
+    return set_error(BH_ERR_UNSUPPORTED, "the tile filter needs D <= 64");
 }
 
 // Any D, any k (bh_knn_general): the same arithmetic and insertion rule,
@@ -504,6 +544,20 @@ static int knn_general_impl(const T *x, int64_t n, int64_t d, int64_t k,
                "kNN workspace too small");
     double *wd = (double *)ws;
     int32_t *wi = (int32_t *)((char *)ws + bh_align(sizeof(double) * n * k));
+    if (std::is_same<T, float>::value && d <= 64 && knn_tile_filter()) {
+        // any k with narrow rows: the tile filter, its lists thread-local
+        // up to kKnnBigK entries and in the scratch beyond
+        const float *xf = (const float *)x;
+        float *of = (float *)out_sqd;
+        if (k <= kKnnMaxK)
+            return knn_tile_dispatch<kKnnMaxK>(xf, n, d, k, out_idx, of, wd,
+                                               wi, bh_cs(stream));
+        if (k <= kKnnBigK)
+            return knn_tile_dispatch<kKnnBigK>(xf, n, d, k, out_idx, of, wd,
+                                               wi, bh_cs(stream));
+        return knn_tile_dispatch<0>(xf, n, d, k, out_idx, of, wd, wi,
+                                    bh_cs(stream));
+    }
     k_knn_general<T><<<bh_blocks(n, kKnnThreads), kKnnThreads, 0,
                        bh_cs(stream)>>>(x, n, (int)d, (int)k, out_idx,
                                         out_sqd, wd, wi);
@@ -546,21 +600,9 @@ static int knn_impl(const T *x, int64_t n, int64_t d, int64_t k,
     if (std::is_same<T, float>::value && knn_f32_filter()) {
         const float *xf = (const float *)x;
         float *of = (float *)out_sqd;
-        static const bool tile = [] {  // BH_KNN_TILE=0: the per-thread filter
-            const char *s = getenv("BH_KNN_TILE");
-            return s ? atoi(s) != 0 : true;
-        }();
-        if (tile) {
-            const int di = (int)d, ki = (int)k;
-            if (d <= 8) return knn_tile_launch<8>(xf, n, di, ki, out_idx, of, st);
-            if (d <= 16) return knn_tile_launch<16>(xf, n, di, ki, out_idx, of, st);
-            if (d <= 24) return knn_tile_launch<24>(xf, n, di, ki, out_idx, of, st);
-            if (d <= 32) return knn_tile_launch<32>(xf, n, di, ki, out_idx, of, st);
-            if (d <= 40) return knn_tile_launch<40>(xf, n, di, ki, out_idx, of, st);
-            if (d <= 48) return knn_tile_launch<48>(xf, n, di, ki, out_idx, of, st);
-            if (d <= 56) return knn_tile_launch<56>(xf, n, di, ki, out_idx, of, st);
-            return knn_tile_launch<64>(xf, n, di, ki, out_idx, of, st);
-        }
+        if (knn_tile_filter())
+            return knn_tile_dispatch<kKnnMaxK>(xf, n, d, k, out_idx, of,
+                                               nullptr, nullptr, st);
         // row widths in steps of 8 (the filter's predicated columns issue
         // whether or not they exist)
         if (d <= 16)

@@ -303,11 +303,14 @@ def test_knn_exact_vs_reference(bh):
 
 
 @pytest.mark.parametrize("n,d,k", [(600, 100, 40), (700, 12, 200),
-                                   (300, 784, 299)])
+                                   (300, 784, 299), (1500, 50, 150),
+                                   (333, 64, 332), (900, 7, 600)])
 def test_knn_general_any_d_and_k(bh, oracle, n, d, k):
     """Beyond bh_knn's D <= 64 / k <= 128 (e.g. perplexity 50+, raw
     784-pixel images): bh_knn_general, the same semantics (f64 column-order
-    sums, ties -> lower id) against the oracle's knn.py restatement."""
+    sums, ties -> lower id) against the oracle's knn.py restatement.
+    float32 rows of D <= 64 take the tile filter with its lists in the
+    scratch (any k); wider rows and float64 the streaming kernel."""
     from paper_2212_11506_b200.knn import knn_exact
     rng = np.random.default_rng(d)
     x = rng.integers(0, 4, (n, d)).astype(np.float32)  # many exact ties
