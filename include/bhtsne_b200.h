@@ -498,6 +498,14 @@ int bh_knn_general_f64(const double *x, int64_t n, int64_t d, int64_t k,
                        int64_t *out_idx, double *out_sqd, void *ws,
                        size_t ws_bytes, bh_stream_t stream);
 /* f64 run mode: float64 data, distances returned as float64. */
+/* float64 data with the float32 tile filter: x32 = x rounded to float32 (the
+ * caller's copy); the same results as bh_knn_f64, bit for bit (the filter
+ * only drops pairs it proves too far; exact sums on the float64 rows).
+ * d <= 64; ws (bh_knn_general_workspace_bytes) only for k > 512, else NULL. */
+int bh_knn_f64_filtered(const double *x, const float *x32, int64_t n,
+                        int64_t d, int64_t k, int64_t *out_idx,
+                        double *out_sqd, void *ws, size_t ws_bytes,
+                        bh_stream_t stream);
 int bh_knn_f64(const double *x, int64_t n, int64_t d, int64_t k,
                int64_t *out_idx, double *out_sqd, bh_stream_t stream);
 

@@ -192,6 +192,7 @@ k_knn_f32(const float *__restrict__ x, int64_t n, int d, int k,
 // The filter is weakest (never wrong) for data far from the origin.
 constexpr int kTileQ = 128, kTileC = 64;   // CTA tile (queries x candidates)
 constexpr float kKnnKappa = 1e-5f;
+constexpr float kKnnKappa64 = 1.1e-5f;  // + the float32 rounding of f64 data
 
 // 4-byte asynchronous global -> shared copy (zero fill when !valid)
 __device__ __forceinline__ void cp_async4(float *smem_dst, const float *gsrc,
@@ -219,11 +220,16 @@ struct KnnTileSmem {
 
 // KCAP: capacity of the thread-local top-k lists (k <= KCAP); 0 = the lists
 // live in caller scratch instead (any k).
-template <int DMAX, int KCAP>
+// OT = double: float64 data (x64) filtered through its float32 copy x --
+// rounding the data moves a distance by at most 4 * 2^-24 (nq + ns), which
+// the wider kKnnKappa64 covers -- with the exact sums on the float64 rows.
+template <int DMAX, int KCAP, typename OT>
 __global__ void __launch_bounds__(kTileQ)
-k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
-           int64_t *__restrict__ out_idx, float *__restrict__ out_sqd,
-           double *__restrict__ ws_d, int32_t *__restrict__ ws_i) {
+k_knn_tile(const float *__restrict__ x, const double *__restrict__ x64,
+           int64_t n, int d, int k, int64_t *__restrict__ out_idx,
+           OT *__restrict__ out_sqd, double *__restrict__ ws_d,
+           int32_t *__restrict__ ws_i) {
+    constexpr bool F64 = std::is_same<OT, double>::value;
     extern __shared__ __align__(16) unsigned char knn_smem[];
     KnnTileSmem<DMAX> &S = *reinterpret_cast<KnnTileSmem<DMAX> *>(knn_smem);
     const int tid = threadIdx.x;
@@ -258,7 +264,7 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
     // this thread's 8 x 8 tile: queries tq4 + {0..3}, 64 + tq4 + {0..3},
     // candidates tc4 + {0..3}, 32 + tc4 + {0..3} (conflict-free LDS.128)
     const int tq4 = (tid & 15) * 4, tc4 = (tid >> 4) * 4;
-    const float om = 1.0f - kKnnKappa;
+    const float om = 1.0f - (F64 ? kKnnKappa64 : kKnnKappa);
     // candidate tiles arrive by cp.async one step ahead of their use
     auto stage = [&](int64_t j0, int buf) {
         // a warp copies whole rows (coalesced reads, conflict-free writes)
@@ -354,11 +360,22 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
                     // overlap; only the ordered sum is a chain): columns past
                     // d are 0 in both tiles and add an exact +0.
                     double e = 0.0;
+                    if (F64) {
+                        const double *__restrict__ xi = x64 + i * d;
+                        const double *__restrict__ xj = x64 + j * d;
+#pragma unroll 4
+                        for (int c = 0; c < d; c++) {
+                            const double diff =
+                                __dsub_rn(__ldg(xi + c), __ldg(xj + c));
+                            e = __dadd_rn(e, __dmul_rn(diff, diff));
+                        }
+                    } else {
 #pragma unroll
-                    for (int c = 0; c < DMAX; c++) {
-                        const double diff = __dsub_rn((double)S.q[c][tid],
-                                                      (double)Sc[r][c]);
-                        e = __dadd_rn(e, __dmul_rn(diff, diff));
+                        for (int c = 0; c < DMAX; c++) {
+                            const double diff = __dsub_rn((double)S.q[c][tid],
+                                                          (double)Sc[r][c]);
+                            e = __dadd_rn(e, __dmul_rn(diff, diff));
+                        }
                     }
                     if (!(e < thr)) continue;
                     // strict-less insertion: before the first entry > e
@@ -397,26 +414,26 @@ k_knn_tile(const float *__restrict__ x, int64_t n, int d, int k,
     if (ok) {
         for (int t = 0; t < k; t++) {
             out_idx[i * k + t] = bi[t];
-            out_sqd[i * k + t] = (float)bd[t];
+            out_sqd[i * k + t] = (OT)bd[t];
         }
     }
 }
 
-template <int DMAX, int KCAP>
-static int knn_tile_launch(const float *x, int64_t n, int d, int k,
-                           int64_t *out_idx, float *out_sqd, double *ws_d,
-                           int32_t *ws_i, cudaStream_t st) {
+template <int DMAX, int KCAP, typename OT>
+static int knn_tile_launch(const float *x, const double *x64, int64_t n,
+                           int d, int k, int64_t *out_idx, OT *out_sqd,
+                           double *ws_d, int32_t *ws_i, cudaStream_t st) {
     const size_t smem = sizeof(KnnTileSmem<DMAX>);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(
-            k_knn_tile<DMAX, KCAP>,
+            k_knn_tile<DMAX, KCAP, OT>,
             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_status(e, "k_knn_tile smem");
         attr_set = true;
     }
-    k_knn_tile<DMAX, KCAP><<<bh_blocks(n, kTileQ), kTileQ, smem, st>>>(
-        x, n, d, k, out_idx, out_sqd, ws_d, ws_i);
+    k_knn_tile<DMAX, KCAP, OT><<<bh_blocks(n, kTileQ), kTileQ, smem, st>>>(
+        x, x64, n, d, k, out_idx, out_sqd, ws_d, ws_i);
     BH_CHECK_LAUNCH("k_knn_tile");
     return BH_OK;
 }
@@ -432,15 +449,16 @@ static bool knn_tile_filter() {
 
 constexpr int kKnnBigK = 512;  // thread-local lists up to this k
 
-template <int KCAP>
-static int knn_tile_dispatch(const float *x, int64_t n, int64_t d, int64_t k,
-                             int64_t *out_idx, float *out_sqd, double *ws_d,
-                             int32_t *ws_i, cudaStream_t st) {
+template <int KCAP, typename OT>
+static int knn_tile_dispatch(const float *x, const double *x64, int64_t n,
+                             int64_t d, int64_t k, int64_t *out_idx,
+                             OT *out_sqd, double *ws_d, int32_t *ws_i,
+                             cudaStream_t st) {
     const int di = (int)d, ki = (int)k;
 #define BH_KNN_TILE_CASE(W)                                                   \
     if (d <= W)                                                               \
-        return knn_tile_launch<W, KCAP>(x, n, di, ki, out_idx, out_sqd,       \
-                                        ws_d, ws_i, st)
+        return knn_tile_launch<W, KCAP, OT>(x, x64, n, di, ki, out_idx,       \
+                                            out_sqd, ws_d, ws_i, st)
     BH_KNN_TILE_CASE(8);
     BH_KNN_TILE_CASE(16);
     BH_KNN_TILE_CASE(24);
@@ -533,6 +551,23 @@ extern "C" size_t bh_knn_general_workspace_bytes(int64_t n, int64_t k) {
     return bh_align(sizeof(double) * n * k) + bh_align(sizeof(int32_t) * n * k);
 }
 
+// The tile filter for any k: thread-local lists up to kKnnBigK entries,
+// caller scratch beyond.
+template <typename OT>
+static int knn_tile_any_k(const float *x, const double *x64, int64_t n,
+                          int64_t d, int64_t k, int64_t *out_idx, OT *out_sqd,
+                          double *wd, int32_t *wi, cudaStream_t st) {
+    if (k <= kKnnMaxK)
+        return knn_tile_dispatch<kKnnMaxK, OT>(x, x64, n, d, k, out_idx,
+                                               out_sqd, wd, wi, st);
+    if (k <= kKnnBigK)
+        return knn_tile_dispatch<kKnnBigK, OT>(x, x64, n, d, k, out_idx,
+                                               out_sqd, wd, wi, st);
+    BH_REQUIRE(wd && wi, "k > %d needs the bh_knn_general workspace", kKnnBigK);
+    return knn_tile_dispatch<0, OT>(x, x64, n, d, k, out_idx, out_sqd, wd, wi,
+                                    st);
+}
+
 template <typename T>
 static int knn_general_impl(const T *x, int64_t n, int64_t d, int64_t k,
                             int64_t *out_idx, T *out_sqd, void *ws,
@@ -549,14 +584,8 @@ static int knn_general_impl(const T *x, int64_t n, int64_t d, int64_t k,
         // up to kKnnBigK entries and in the scratch beyond
         const float *xf = (const float *)x;
         float *of = (float *)out_sqd;
-        if (k <= kKnnMaxK)
-            return knn_tile_dispatch<kKnnMaxK>(xf, n, d, k, out_idx, of, wd,
-                                               wi, bh_cs(stream));
-        if (k <= kKnnBigK)
-            return knn_tile_dispatch<kKnnBigK>(xf, n, d, k, out_idx, of, wd,
-                                               wi, bh_cs(stream));
-        return knn_tile_dispatch<0>(xf, n, d, k, out_idx, of, wd, wi,
-                                    bh_cs(stream));
+        return knn_tile_any_k<float>(xf, nullptr, n, d, k, out_idx, of, wd, wi,
+                                     bh_cs(stream));
     }
     k_knn_general<T><<<bh_blocks(n, kKnnThreads), kKnnThreads, 0,
                        bh_cs(stream)>>>(x, n, (int)d, (int)k, out_idx,
@@ -601,8 +630,8 @@ static int knn_impl(const T *x, int64_t n, int64_t d, int64_t k,
         const float *xf = (const float *)x;
         float *of = (float *)out_sqd;
         if (knn_tile_filter())
-            return knn_tile_dispatch<kKnnMaxK>(xf, n, d, k, out_idx, of,
-                                               nullptr, nullptr, st);
+            return knn_tile_dispatch<kKnnMaxK, float>(
+                xf, nullptr, n, d, k, out_idx, of, nullptr, nullptr, st);
         // row widths in steps of 8 (the filter's predicated columns issue
         // whether or not they exist)
         if (d <= 16)
@@ -640,4 +669,26 @@ extern "C" int bh_knn(const float *x, int64_t n, int64_t d, int64_t k,
 extern "C" int bh_knn_f64(const double *x, int64_t n, int64_t d, int64_t k,
                           int64_t *out_idx, double *out_sqd, bh_stream_t stream) {
     return knn_impl(x, n, d, k, out_idx, out_sqd, stream);
+}
+
+extern "C" int bh_knn_f64_filtered(const double *x, const float *x32,
+                                   int64_t n, int64_t d, int64_t k,
+                                   int64_t *out_idx, double *out_sqd, void *ws,
+                                   size_t ws_bytes, bh_stream_t stream) {
+    BH_REQUIRE(x && x32 && out_idx && out_sqd, "null argument");
+    BH_REQUIRE(k >= 1 && k <= n - 1, "k must be in [1, %lld], got %lld",
+               (long long)(n - 1), (long long)k);
+    BH_REQUIRE(d >= 1 && d <= 64,
+               "bh_knn_f64_filtered supports 1 <= D <= 64, got %lld",
+               (long long)d);
+    double *wd = nullptr;
+    int32_t *wi = nullptr;
+    if (k > kKnnBigK) {
+        BH_REQUIRE(ws && ws_bytes >= bh_knn_general_workspace_bytes(n, k),
+                   "kNN workspace too small");
+        wd = (double *)ws;
+        wi = (int32_t *)((char *)ws + bh_align(sizeof(double) * n * k));
+    }
+    return knn_tile_any_k<double>(x32, x, n, d, k, out_idx, out_sqd, wd, wi,
+                                  bh_cs(stream));
 }

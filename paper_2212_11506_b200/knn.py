@@ -19,6 +19,13 @@ from .affinity import NeighborGraph
 # k <= 128 and D <= 64; bh_knn_general any k and D (slower)
 MAX_K = 128
 MAX_D = 64
+BIG_K = 512  # bh_knn_f64_filtered keeps its lists thread-local up to here
+
+
+def _f64_filter() -> bool:
+    """BH_KNN_TILE=0 keeps the per-thread float64 kernel (A/B)."""
+    import os
+    return os.environ.get("BH_KNN_TILE", "1") != "0"
 
 
 def knn_exact(x, k: int) -> NeighborGraph:
@@ -33,7 +40,16 @@ def knn_exact(x, k: int) -> NeighborGraph:
         raise ValueError(f"k must be in [1, {n - 1}], got {k}")
     idx = torch.empty((n, k), dtype=torch.int64, device=data.device)
     sqd = torch.empty((n, k), dtype=dt, device=data.device)
-    if k <= MAX_K and d <= MAX_D:
+    if dt == torch.float64 and d <= MAX_D and _f64_filter():
+        # float64 data: the float32 tile filter on a rounded copy, exact
+        # sums on the float64 rows (the same graph, bit for bit)
+        lib = _lib.load()
+        ws = (_lib.workspace(lib.bh_knn_general_workspace_bytes(n, k))
+              if k > BIG_K else None)
+        call("bh_knn_f64_filtered", ptr(data), ptr(data.to(torch.float32)),
+             n, d, k, ptr(idx), ptr(sqd), ptr(ws) if ws is not None else None,
+             ws.numel() if ws is not None else 0, stream())
+    elif k <= MAX_K and d <= MAX_D:
         call(_lib.fn("bh_knn", dt), ptr(data), n, d, k, ptr(idx), ptr(sqd),
              stream())
     else:  # any D / k: columns in chunks, the top-k list in scratch
