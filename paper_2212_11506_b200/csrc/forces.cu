@@ -574,16 +574,19 @@ k_repulsive_exact(const float2 *__restrict__ y, int64_t n,
             s_y[q] = j0 + q < n ? y[j0 + q] : make_float2(0.f, 0.f);
         __syncthreads();
         const int nb = (n - j0) < kExTile ? (int)(n - j0) : kExTile;
+        // (the same pair arithmetic as the traversal: rcp.approx, FMA)
+        const int qself = (i >= j0 && i < j0 + kExTile) ? (int)(i - j0) : -1;
         float fz = 0.f, fx = 0.f, fy = 0.f;
+#pragma unroll 4
         for (int q = 0; q < nb; q++) {
             const float2 p = s_y[q];
-            float dx = yi.x - p.x, dy = yi.y - p.y;
-            float k = __frcp_rn(1.0f + dx * dx + dy * dy);
-            if (j0 + q == i) k = 0.f;
-            float k2 = k * k;
+            const float dx = yi.x - p.x, dy = yi.y - p.y;
+            float k = rcp_approx(1.0f + fmaf(dx, dx, dy * dy));
+            k = q == qself ? 0.f : k;
+            const float k2 = k * k;
             fz += k;
-            fx += k2 * dx;
-            fy += k2 * dy;
+            fx = fmaf(k2, dx, fx);
+            fy = fmaf(k2, dy, fy);
         }
         z += (double)fz;
         r0 += (double)fx;
