@@ -223,8 +223,11 @@ struct KnnTileSmem {
 // OT = double: float64 data (x64) filtered through its float32 copy x --
 // rounding the data moves a distance by at most 4 * 2^-24 (nq + ns), which
 // the wider kKnnKappa64 covers -- with the exact sums on the float64 rows.
+#ifndef BH_KNN_MINB
+#define BH_KNN_MINB 3  // shared memory allows 3 CTAs/SM: up to 168 registers
+#endif
 template <int DMAX, int KCAP, typename OT>
-__global__ void __launch_bounds__(kTileQ)
+__global__ void __launch_bounds__(kTileQ, BH_KNN_MINB)
 k_knn_tile(const float *__restrict__ x, const double *__restrict__ x64,
            int64_t n, int d, int k, int64_t *__restrict__ out_idx,
            OT *__restrict__ out_sqd, double *__restrict__ ws_d,
@@ -297,7 +300,11 @@ k_knn_tile(const float *__restrict__ x, const double *__restrict__ x64,
         for (int a = 0; a < 8; a++)
 #pragma unroll
             for (int b = 0; b < 8; b++) acc[a][b] = 0.f;
-#pragma unroll 2
+#ifndef BH_KNN_UNROLL
+#define BH_KNN_UNROLL 7  // 1 / 2 / 4 / 7 / 14 at C3: 6.59 / 6.28 / 5.97 / 5.89 / 6.61 s
+#endif
+        constexpr int kUnroll = BH_KNN_UNROLL;
+#pragma unroll kUnroll
         for (int c = 0; c < DMAX; c += 2) {
             // two columns per round: 8 broadcast LDS.64 of the candidates'
             // rows, 2 + 2 LDS.128 of the transposed queries
