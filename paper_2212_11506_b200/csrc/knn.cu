@@ -190,7 +190,12 @@ k_knn_f32(const float *__restrict__ x, int64_t n, int d, int k,
 // through k_knn's exact f64 column-order sum and strict-less insertion, so
 // the kept set, the distances and the tie order are k_knn's, bit for bit.
 // The filter is weakest (never wrong) for data far from the origin.
-constexpr int kTileQ = 128, kTileC = 64;   // CTA tile (queries x candidates)
+#ifndef BH_KNN_TILEQ
+#define BH_KNN_TILEQ 128  // queries (= threads) per CTA: 128 or 256
+#endif
+constexpr int kTileQ = BH_KNN_TILEQ, kTileC = 64;  // CTA tile (queries x candidates)
+constexpr int kTileQH = kTileQ / 2;                // a thread's second query quad
+constexpr int kTileTQ = kTileQ / 8;                // threads along the queries
 constexpr float kKnnKappa = 1e-5f;
 constexpr float kKnnKappa64 = 1.1e-5f;  // + the float32 rounding of f64 data
 
@@ -224,7 +229,7 @@ struct KnnTileSmem {
 // rounding the data moves a distance by at most 4 * 2^-24 (nq + ns), which
 // the wider kKnnKappa64 covers -- with the exact sums on the float64 rows.
 #ifndef BH_KNN_MINB
-#define BH_KNN_MINB 3  // shared memory allows 3 CTAs/SM: up to 168 registers
+#define BH_KNN_MINB (BH_KNN_TILEQ == 128 ? 3 : 2)  // the shared-memory limit; 128-thread CTAs: up to 168 registers
 #endif
 template <int DMAX, int KCAP, typename OT>
 __global__ void __launch_bounds__(kTileQ, BH_KNN_MINB)
@@ -266,7 +271,7 @@ k_knn_tile(const float *__restrict__ x, const double *__restrict__ x64,
     double thr = INFINITY;
     // this thread's 8 x 8 tile: queries tq4 + {0..3}, 64 + tq4 + {0..3},
     // candidates tc4 + {0..3}, 32 + tc4 + {0..3} (conflict-free LDS.128)
-    const int tq4 = (tid & 15) * 4, tc4 = (tid >> 4) * 4;
+    const int tq4 = (tid % kTileTQ) * 4, tc4 = (tid / kTileTQ) * 4;
     const float om = 1.0f - (F64 ? kKnnKappa64 : kKnnKappa);
     // candidate tiles arrive by cp.async one step ahead of their use
     auto stage = [&](int64_t j0, int buf) {
@@ -318,7 +323,7 @@ k_knn_tile(const float *__restrict__ x, const double *__restrict__ x64,
                 const float4 qa =
                     *reinterpret_cast<const float4 *>(&S.q[c + h][tq4]);
                 const float4 qb =
-                    *reinterpret_cast<const float4 *>(&S.q[c + h][64 + tq4]);
+                    *reinterpret_cast<const float4 *>(&S.q[c + h][kTileQH + tq4]);
                 const float qv[8] = {qa.x, qa.y, qa.z, qa.w,
                                      qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
@@ -333,7 +338,7 @@ k_knn_tile(const float *__restrict__ x, const double *__restrict__ x64,
         // filter: flag the pairs that may enter
 #pragma unroll
         for (int a = 0; a < 8; a++) {
-            const int ql = (a < 4 ? tq4 : 60 + tq4) + a;  // 64 + tq4 + (a - 4)
+            const int ql = (a < 4 ? tq4 : kTileQH - 4 + tq4) + a;
             const float nqa = S.nq[ql], th = S.thr[ql];
             unsigned m0 = 0u, m1 = 0u;
 #pragma unroll
