@@ -78,6 +78,25 @@ def test_knn_matches_brute_force(bh, rng, dtype):
                                       sqd.astype(np.float32))
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("offset,scale", [(1e4, 1.0), (1e6, 1.0), (0.0, 1e-20),
+                                          (0.0, 1e25)])
+def test_knn_filter_is_only_a_filter(bh, rng, dtype, offset, scale):
+    """The f32 dot-product filter (k_knn_tile) may only drop pairs it proves
+    too far: data far from the origin (|x|^2 >> d^2, where its bound is
+    weakest), tiny values (f32 underflow of the norms) and huge ones (f32
+    overflow -> NaN bounds, every pair taken exactly) still give the
+    brute-force graph bit for bit."""
+    if dtype == np.float32 and scale > 1e18:
+        pytest.skip("squared distances overflow float32 itself")
+    n, d, k = 700, 20, 30
+    data = ((rng.standard_normal((n, d)) + offset) * scale).astype(dtype)
+    g = bh.knn_exact(data, k)
+    idx, sqd = brute_force(data.astype(np.float64), k)
+    np.testing.assert_array_equal(host(g.indices), idx)
+    np.testing.assert_array_equal(host(g.sq_distances), sqd.astype(dtype))
+
+
 def test_knn_rows_sorted_valid_and_bounding(bh, rng):
     data = rng.standard_normal((100, 4))
     k = 10
