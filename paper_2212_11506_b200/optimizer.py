@@ -385,8 +385,10 @@ class Engine:
         # fraction of the share's CSR rows swept on the (low-priority) side
         # stream under the latency-bound tree build; the rest run inside the
         # fused force launch.  Measured at C3 (it/s, round 1): 0: 487, 0.2:
-        # 612, 0.25: 614, 0.3: 619, 0.35: 620, 0.4: 618, 0.45: 613, 0.55: 602
-        self._attr_split = 0.35
+        # 612, 0.25: 614, 0.3: 619, 0.35: 620, 0.4: 618, 0.45: 613, 0.55: 602;
+        # final tree, full schedule / the driver's window: 0.275: 660.9 / 634,
+        # 0.3: 662.6 / 637.1, 0.325: 662.8 / 637.6, 0.35: 661.2 / 636.9
+        self._attr_split = 0.325
         self._partition()
         if shard is not None:
             shard.attach(self)
